@@ -1,0 +1,341 @@
+#!/usr/bin/env python3
+"""Benchmark of the road-surface stereo hot path (arXiv 1807.07433) on B200.
+
+Workload (BASELINE.json configs[4] = "c5", the metric's 1280x720x64d shape):
+each rank processes a batch of --batch synthetic 1280x720 stereo pairs per step
+(warp -> NCC dual volumes -> bilateral aggregation of both -> WTA + LR check +
+parabola -> triangulation), frames drawn from a pool of distinct seeded frames;
+with N > 1 ranks the per-rank disparity maps are gathered to rank 0 over NCCL
+(configs[4]).  Weak scaling: per-rank work is fixed.
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the fp64 CPU oracle
+(oracle/, test infrastructure) on bounded samples of the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.45: SMs x FP32 lanes x 2 x max SM clock
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=8, help="frames per rank per step")
+    ap.add_argument("--pool", type=int, default=16, help="distinct input frames per rank")
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--impl", default="rsr", choices=["rsr", "reference"])
+    ap.add_argument("--no-gather", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=16, help="oracle sample: rows of one frame")
+    return ap.parse_args()
+
+
+def workload_config(cfg, args, extra=None):
+    d = {"workload": f"{cfg.name}: {cfg.width}x{cfg.height} uint8 pairs, D={cfg.D} [{cfg.d_lo},{cfg.d_hi}], "
+                     f"NCC {2 * cfg.rho_block + 1}x{2 * cfg.rho_block + 1}, bilateral "
+                     f"{2 * cfg.rho_agg + 1}x{2 * cfg.rho_agg + 1} (gamma_d={cfg.gamma_d}, gamma_r={cfg.gamma_r}), "
+                     f"LRC tol {cfg.lrc_tol}, subpixel, triangulation",
+         "frames_per_rank_per_step": args.batch, "width": cfg.width, "height": cfg.height, "D": cfg.D,
+         "l2": "per-step working set (4 fp32 volumes x batch = GBs) >> 126 MB L2; inputs cycle a pool "
+               f"of {args.pool} distinct frames per rank"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+def oracle_sample(cfg, rows, frame_index=0):
+    """Time the fp64 oracle on `rows` rows of one frame; return (seconds, frames)."""
+    from oracle import rsr_oracle as O
+    f = synth.make_frame(cfg, frame_index)
+    r0 = cfg.height // 2 - rows // 2
+    t0 = time.perf_counter()
+    O.run_pipeline(f.left, f.right, f.alpha, f.beta, cfg, rows=(r0, r0 + rows), keep_volumes=False)
+    dt = time.perf_counter() - t0
+    return dt, rows / cfg.height
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count()
+
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    samples = []
+    frames = 0.0
+    t_total = 0.0
+    for i in range(args.warmup + args.steps):
+        dt, fr = oracle_sample(cfg, args.cpu_rows, frame_index=i % args.pool)
+        if i >= args.warmup:
+            samples.append(dt)
+            frames += fr
+            t_total += dt
+    value = frames / t_total
+    D = cfg.D
+    line = {
+        "impl": "reference", "metric": "fps", "value": value, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "gde_per_s": value * cfg.width * cfg.height * D / 1e9,
+        "config": workload_config(cfg, args, {"sample": f"oracle on {args.cpu_rows} rows of one frame per step"}),
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{args.cpu_rows} of {cfg.height} rows of one 1280x720 frame per step "
+                                   "(NumPy fp64, single process)"},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = synth.get_config(args.config)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1807_07433_b200 as rsr
+
+    assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    B, H, W = args.batch, cfg.height, cfg.width
+    params = rsr.StereoParams.from_config(cfg)
+    pipe = rsr.StereoPipeline(B, H, W, params, device=dev)
+
+    # ---- inputs: a pool of distinct seeded frames per rank, resident in HBM ----
+    pool = args.pool
+    idx = [rank * pool + i for i in range(pool)]
+    left_np, right_np, ab_np = synth.make_batch(cfg, idx)
+    left = torch.from_numpy(left_np).to(dev)
+    right = torch.from_numpy(right_np).to(dev)
+    ab = torch.from_numpy(ab_np).to(dev)
+    nbatches = pool // B
+    assert nbatches >= 1, "--pool must be >= --batch"
+
+    gather_list = None
+    if world > 1 and not args.no_gather and rank == 0:
+        gather_list = [torch.empty((B, H, W), dtype=torch.float32, device=dev) for _ in range(world)]
+
+    stream = torch.cuda.current_stream()
+    ev = {k: [] for k in ("agg0", "agg1", "agg2", "agg3", "cost0", "cost1", "disp0", "disp1")}
+
+    def step(i, record=False):
+        sl = slice((i % nbatches) * B, (i % nbatches) * B + B)
+        L, R, A = left[sl], right[sl], ab[sl]
+        p = pipe.p
+        rsr.rsr_warp(R, A, pipe.warped, pipe.valid, pipe.shift)
+        if record:
+            e = torch.cuda.Event(enable_timing=True); e.record(stream); ev["cost0"].append(e)
+        rsr.rsr_cost_volume(L, pipe.warped, pipe.valid, p.rho_block, p.d_lo, p.d_hi, vol_ref=pipe.vol_ref,
+                            vol_tar=pipe.vol_tar, nan_ref=pipe.nan_ref, nan_tar=pipe.nan_tar,
+                            workspace=pipe.workspace)
+        if record:
+            e = torch.cuda.Event(enable_timing=True); e.record(stream); ev["cost1"].append(e)
+            e = torch.cuda.Event(enable_timing=True); e.record(stream); ev["agg0"].append(e)
+        rsr.rsr_aggregate(pipe.vol_ref, L, p.rho_agg, p.gamma_d, p.gamma_r, pipe.nan_ref, pipe.agg_ref)
+        if record:
+            e = torch.cuda.Event(enable_timing=True); e.record(stream); ev["agg1"].append(e)
+            e = torch.cuda.Event(enable_timing=True); e.record(stream); ev["agg2"].append(e)
+        rsr.rsr_aggregate(pipe.vol_tar, pipe.warped, p.rho_agg, p.gamma_d, p.gamma_r, pipe.nan_tar, pipe.agg_tar)
+        if record:
+            e = torch.cuda.Event(enable_timing=True); e.record(stream); ev["agg3"].append(e)
+            e = torch.cuda.Event(enable_timing=True); e.record(stream); ev["disp0"].append(e)
+        rsr.rsr_disparity(pipe.agg_ref, pipe.agg_tar, pipe.shift, p.d_lo, p.d_hi, p.lrc_tol, True,
+                          pipe.disparity)
+        if record:
+            e = torch.cuda.Event(enable_timing=True); e.record(stream); ev["disp1"].append(e)
+        rsr.rsr_reconstruct(pipe.disparity, p.focal, p.baseline, d_min=p.d_min, xyz=pipe.xyz)
+        if world > 1 and not args.no_gather:
+            dist.gather(pipe.disparity, gather_list, dst=0)
+
+    launches_per_step = 1 + 2 + 2 * ((cfg.D + 127) // 128) + 2 + 1 + 1
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    with ClockSampler(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(args.steps):
+            step(args.warmup + i, record=True)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    def avg_ms(a, b):
+        return statistics.mean(x.elapsed_time(y) for x, y in zip(ev[a], ev[b]))
+
+    agg_ms = (avg_ms("agg0", "agg1") + avg_ms("agg2", "agg3")) / 2
+    cost_ms = avg_ms("cost0", "cost1")
+    disp_ms = avg_ms("disp0", "disp1")
+    frames = B * args.steps * world
+    fps = frames / (ms / 1e3)
+    ms_step = ms / args.steps
+    agg_flop = B * H * W * cfg.D * (2 * cfg.rho_agg + 1) ** 2 * 2
+    achieved = agg_flop / (agg_ms / 1e3) / 1e12
+
+    # ---- end-to-end: host (pinned) inputs -> H2D -> five C-ABI calls -> D2H disparity ----
+    e2e = None
+    if not args.no_e2e:
+        hl = torch.from_numpy(left_np[:B]).pin_memory()
+        hr = torch.from_numpy(right_np[:B]).pin_memory()
+        hab = torch.from_numpy(ab_np[:B]).pin_memory()
+        hout = torch.empty((B, H, W), dtype=torch.float32).pin_memory()
+        dl = torch.empty_like(left[:B]); dr = torch.empty_like(right[:B]); dab = torch.empty_like(ab[:B])
+
+        def e2e_step():
+            dl.copy_(hl, non_blocking=True); dr.copy_(hr, non_blocking=True); dab.copy_(hab, non_blocking=True)
+            pipe.run(dl, dr, dab, with_wta=False)
+            hout.copy_(pipe.disparity, non_blocking=True)
+
+        for _ in range(args.warmup):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ems = a0.elapsed_time(a1)
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": frames / (ems / 1e3), "unit": "frames/s",
+               "h2d_bytes_per_step": int(hl.numel() + hr.numel() + hab.numel() * 8),
+               "d2h_bytes_per_step": int(hout.numel() * 4)}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        dt, fr = oracle_sample(cfg, args.cpu_rows)
+        cpu = {"value": fr / dt, "unit": "frames/s", "cores": 1, "kind": "oracle",
+               "sample": f"{args.cpu_rows} of {H} rows of one {W}x{H} frame (NumPy fp64, single process), "
+                         f"{dt:.1f} s; host has {host_cores()} cores"}
+
+    line = {
+        "metric": "fps", "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "gde_per_s": fps * W * H * cfg.D / 1e9,
+        "config": workload_config(cfg, args, {"parallelism": f"frames dp{world}" +
+                                              ("" if world == 1 or args.no_gather else " + NCCL gather")}),
+        "roofline": {"kernel": "k_aggregate (rsr_aggregate, Eq. 8)", "bound": "alu", "achieved": achieved,
+                     "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
+                     "traffic": None,
+                     "peak_note": "FP32 FMA: 148 SMs x 128 lanes x 2 flop x 1965 MHz (B200_PROFILING.md unit "
+                                  "counts and max clock); measured FFMA-chain peak 71.5 TFLOP/s "
+                                  "(profiles/r01_ubench_fp32_lds.jsonl)",
+                     "algorithmic_flop_per_launch": agg_flop, "ms_per_launch": agg_ms,
+                     "share_of_step": 2 * agg_ms / ms_step},
+        "kernel_ms": {"cost_volume": cost_ms, "aggregate_each": agg_ms, "disparity": disp_ms},
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,190 @@
+/*
+ * rsr.h — C ABI of the B200-native road-surface stereo hot path
+ * (arXiv 1807.07433, "Real-Time Stereo Vision for Road Surface 3-D
+ * Reconstruction").  P:NN below = line NN of the paper's LaTeX.
+ *
+ * Five calls, in the paper's order (Fig. 1):
+ *   rsr_warp         perspective transformation of the target image   (Eq. 2)
+ *   rsr_cost_volume  NCC costs into the reference / target volumes    (Eqs. 3-5)
+ *   rsr_aggregate    bilateral cost aggregation (FBS), one volume      (Eqs. 8-10)
+ *   rsr_disparity    WTA + left-right check + parabola + post-process  (Eqs. 11-12)
+ *   rsr_reconstruct  triangulation Z = f b / d
+ *
+ * Conventions (all calls):
+ *  - Every array argument is a DEVICE pointer (CUDA global memory) unless
+ *    stated otherwise.  The caller allocates and owns all memory; the library
+ *    never allocates, frees or synchronises.  Each call only enqueues kernels
+ *    on `stream` (a cudaStream_t passed as void*; NULL = legacy default stream)
+ *    and returns; errors of the asynchronous kernels surface on the caller's
+ *    next synchronisation.
+ *  - Layout: dense, row-major, batch-major.  Images / maps are [B][H][W];
+ *    cost and aggregated volumes are [B][H][W][D] fp32 with the disparity
+ *    index k = r - d_lo innermost (each pixel's D costs are contiguous);
+ *    points are [B][H][W][3] fp32 (X, Y, Z).
+ *  - Invalid entries are values, not errors: quiet NaN in float outputs,
+ *    -1 in int16 index maps.
+ *  - All argument validation happens before any launch: a call that returns
+ *    an error code has enqueued nothing and written nothing.
+ *  - Results are bitwise deterministic for identical inputs, independent of
+ *    batch size and of the number of GPUs (no atomics on floats).
+ *  - Thread safety: calls are re-entrant; concurrent calls on different
+ *    streams with disjoint outputs are safe.
+ */
+#ifndef RSR_H
+#define RSR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (mirror the exit-code convention of SPEC S:531). */
+typedef enum {
+  RSR_OK = 0,
+  RSR_E_ARG = 2,      /* null required pointer, bad dimension or parameter      */
+  RSR_E_DATA = 3,     /* data too small for the requested window               */
+  RSR_E_INTERNAL = 4  /* CUDA launch error (cudaGetLastError after a launch)    */
+} rsr_status;
+
+typedef struct {
+  int32_t batch;   /* B >= 1 independent frames                              */
+  int32_t height;  /* H >= 1 rows (v)                                        */
+  int32_t width;   /* W >= 1 columns (u)                                     */
+} rsr_shape;
+
+/* ------------------------------------------------------------------------ */
+/* Step 1 — perspective transformation.                               */
+/* Row v of the target image is shifted right by s(v) = floor(alpha*v + beta  */
+/* + 1/2) (fp64 multiply, then two fp64 adds, no FMA contraction):           */
+/*   warped[b][v][u] = target[b][v][u - s(v)]  if 0 <= u - s(v) < W, else 0   */
+/*   valid [b][v][u] = 1 in the first case, 0 otherwise.                      */
+/* alpha = slope in px/row (the paper's alpha_1), beta = intercept in px     */
+/* (alpha_0); the paper's delta is absorbed into the signed residual    */
+/* search range of rsr_cost_volume.                                           */
+/*   alpha_beta : double [B][2] {alpha, beta} per frame                       */
+/*   target     : uint8  [B][H][W] target (right) image i_r                   */
+/*   warped     : uint8  [B][H][W] out                                        */
+/*   valid      : uint8  [B][H][W] out, 0/1                                   */
+/*   shift      : int32  [B][H]    out, s(v) clamped to [-2^30, 2^30]         */
+/* Errors: RSR_E_ARG on a NULL pointer or non-positive dimension.            */
+int rsr_warp(rsr_shape s, const double* alpha_beta, const uint8_t* target,
+             uint8_t* warped, uint8_t* valid, int32_t* shift, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Step 2 — NCC cost volumes (Eqs. 3-5).                           */
+/* For r in [d_lo, d_hi], k = r - d_lo, n = (2 rho_block + 1)^2:             */
+/*   c(u,v,r) = (n S_lw - S_l S_w) / sqrt((n S_ll - S_l^2)(n S_ww - S_w^2)), */
+/* the integer-sum form of Eq. (3) with Eqs. (4)-(5); left block centred at  */
+/* (u, v) in `ref`, right block at (u - r, v) in `warped`.  c is clamped to  */
+/* [-1, 1].  NaN if either block leaves the image, the right block holds a   */
+/* pixel with valid == 0, or either block is constant (exact integer test).  */
+/*   vol_ref[b][v][u][k]  = c(u, v, r)         (reference volume)      */
+/*   vol_tar[b][v][u'][k] = c(u' + r, v, r)    (target volume)         */
+/* The two are bitwise consistent: vol_tar[v][u-r][k] == vol_ref[v][u][k].    */
+/* nan_ref / nan_tar (optional, uint8 [B][H][W]) summarise each pixel's D    */
+/* costs: bit 0 = some k is NaN, bit 1 = some k is finite (so 1 = all NaN,    */
+/* 3 = partly NaN).  rsr_aggregate uses them to skip per-disparity validity   */
+/* bookkeeping wherever no pixel of a tile is partly NaN.                     */
+/*   workspace : device scratch of rsr_cost_workspace_size(s) bytes, 16-byte  */
+/*               aligned, owned by the caller (per-pixel block sums / norms). */
+/* Errors: RSR_E_ARG on NULL ref/warped/valid/vol_ref/workspace, rho_block   */
+/* < 1 or > 7, d_hi < d_lo, D > 32767, workspace too small;                  */
+/* RSR_E_DATA if H or W < 2 rho_block + 1.                                   */
+typedef struct {
+  int32_t rho_block;  /* varrho, NCC half window (block = 2 varrho + 1)       */
+  int32_t d_lo;       /* smallest residual disparity (signed)                 */
+  int32_t d_hi;       /* largest residual disparity; D = d_hi - d_lo + 1       */
+} rsr_cost_params;
+
+size_t rsr_cost_workspace_size(rsr_shape s);
+
+int rsr_cost_volume(rsr_shape s, rsr_cost_params p, const uint8_t* ref,
+                    const uint8_t* warped, const uint8_t* valid,
+                    float* vol_ref, float* vol_tar, uint8_t* nan_ref,
+                    uint8_t* nan_tar, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Step 3 — bilateral cost aggregation, Eq. (8) with Eqs. (9)-(10)           */
+/* (P:138-150), applied to one volume (call it for the reference volume with */
+/* guide = ref and for the target volume with guide = warped):               */
+/*   out[b][v][u][k] = sum_t w_t vol[b][v+dy][u+dx][k] / sum_t w_t            */
+/*   w_t = exp(-(dx^2+dy^2)/gamma_d^2) * exp(-(g(u+dx,v+dy) - g(u,v))^2/gamma_r^2) */
+/* over |dx|,|dy| <= rho, skipping taps outside the image or with a NaN cost; */
+/* out is NaN iff vol[b][v][u][k] is NaN.  gamma_r may be +inf (w_r = 1).     */
+/*   vol     : float [B][H][W][D], NaN = invalid                              */
+/*   guide   : uint8 [B][H][W]                                                */
+/*   nan_map : optional uint8 [B][H][W] in the rsr_cost_volume encoding       */
+/*             (bit 0 some k NaN, bit 1 some k finite); it must describe vol  */
+/*             exactly.  NULL = assume any pixel may be partly NaN (correct,  */
+/*             slower).                                                       */
+/*   out     : float [B][H][W][D]; must not alias vol                         */
+/* Errors: RSR_E_ARG on NULL vol/guide/out, D < 1 or > 32767, rho < 0 or      */
+/* > 10, gamma_d <= 0 or NaN, gamma_r <= 0 or NaN.                            */
+typedef struct {
+  int32_t rho;      /* rho, aggregation half window (window = 2 rho + 1)      */
+  float gamma_d;    /* spatial parameter of Eq. (9)                           */
+  float gamma_r;    /* range parameter of Eq. (10), may be +inf               */
+} rsr_agg_params;
+
+int rsr_aggregate(rsr_shape s, int32_t D, rsr_agg_params p, const float* vol,
+                  const uint8_t* guide, const uint8_t* nan_map, float* out,
+                  void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Steps 4-5 — WTA, left-right consistency, parabola subpixel and            */
+/* post-processing.                                              */
+/*   k_L(u,v) = smallest k maximising agg_ref over non-NaN entries (-1 if     */
+/*   none); k_R likewise on agg_tar (WTA, "highest correlation" P:46). */
+/*   Keep (u,v) iff k_L >= 0, u' = u - (k_L + d_lo) in [0, W), k_R(u',v) >= 0 */
+/*   and |k_L - k_R(u',v)| <= lrc_tol (Eq. 11).                    */
+/*   r_s = r + (a - c) / (2a + 2c - 4b), a,b,c = agg_ref[k_L-1, k_L, k_L+1],   */
+/*   when subpixel != 0, 1 <= k_L <= D-2, a and c are not NaN and          */
+/*   |2a + 2c - 4b| > 1e-12 (Eq. 12); else r_s = r = k_L + d_lo.  */
+/*   disparity[b][v][u] = r_s + shift[b][v], NaN if not kept.         */
+/*   agg_ref, agg_tar : float [B][H][W][D] aggregated volumes                 */
+/*   shift            : int32 [B][H] from rsr_warp                            */
+/*   disparity        : float [B][H][W] out                                   */
+/*   wta_ref, wta_tar : optional int16 [B][H][W] out (k_L, k_R; -1 invalid)   */
+/* Errors: RSR_E_ARG on NULL required pointers, d_hi < d_lo, D > 32767,      */
+/* lrc_tol < 0, W > 32768 (one CTA holds a row of k_R in shared memory).      */
+typedef struct {
+  int32_t d_lo, d_hi;  /* residual search range, as in rsr_cost_params         */
+  int32_t lrc_tol;     /* tau >= 0                                             */
+  int32_t subpixel;    /* 0 = integer disparities, 1 = parabola refinement     */
+} rsr_disp_params;
+
+int rsr_disparity(rsr_shape s, rsr_disp_params p, const float* agg_ref,
+                  const float* agg_tar, const int32_t* shift, float* disparity,
+                  int16_t* wta_ref, int16_t* wta_tar, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Step 5b — triangulation (the paper gives no formula: rectified  */
+/* pinhole).  For d = disparity[b][v][u] > d_min:                            */
+/*   Z = f * baseline / d,  X = (u - u0) * Z / f,  Y = (v - v0) * Z / f       */
+/* else (d <= d_min or NaN) the point is (NaN, NaN, NaN).                     */
+/*   disparity : float [B][H][W];  xyz : float [B][H][W][3] out (metres)      */
+/* Errors: RSR_E_ARG on NULL pointers, f <= 0, baseline <= 0, d_min <= 0.     */
+typedef struct {
+  double f;         /* focal length, px                                       */
+  double baseline;  /* T_c, metres                                            */
+  double u0, v0;    /* principal point, px                                    */
+  double d_min;     /* smallest triangulated disparity, px (> 0)              */
+} rsr_rig;
+
+int rsr_reconstruct(rsr_shape s, rsr_rig rig, const float* disparity,
+                    float* xyz, void* stream);
+
+/* Human-readable text for a status code (static storage). */
+const char* rsr_strerror(int status);
+
+/* Library version as MAJOR*10000 + MINOR*100 + PATCH. */
+int rsr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RSR_H */

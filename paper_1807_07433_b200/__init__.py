@@ -1,0 +1,11 @@
+"""B200-native (sm_100a) road-surface stereo hot path of arXiv 1807.07433.
+
+The computation lives in librsr.so (CUDA kernels behind the C ABI of
+include/rsr.h); this package is the thin Python binding (ops.py) plus buffer
+plumbing (pipeline.py).  PyTorch supplies device memory, streams and
+torch.distributed only.
+"""
+from ._lib import RsrError, lib  # noqa: F401
+from .ops import (rsr_aggregate, rsr_cost_volume, rsr_disparity, rsr_reconstruct,  # noqa: F401
+                  rsr_warp, cost_workspace_bytes)
+from .pipeline import StereoParams, StereoPipeline  # noqa: F401

@@ -1,0 +1,77 @@
+"""ctypes binding of librsr.so (include/rsr.h).  Argument marshalling only:
+every step of the path runs in the library's CUDA kernels.  There is no CPU
+fallback: if the shared library is missing or a tensor is not on a CUDA device,
+calls raise."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librsr.so")
+
+RSR_OK, RSR_E_ARG, RSR_E_DATA, RSR_E_INTERNAL = 0, 2, 3, 4
+
+
+class RsrShape(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("height", ctypes.c_int32), ("width", ctypes.c_int32)]
+
+
+class RsrCostParams(ctypes.Structure):
+    _fields_ = [("rho_block", ctypes.c_int32), ("d_lo", ctypes.c_int32), ("d_hi", ctypes.c_int32)]
+
+
+class RsrAggParams(ctypes.Structure):
+    _fields_ = [("rho", ctypes.c_int32), ("gamma_d", ctypes.c_float), ("gamma_r", ctypes.c_float)]
+
+
+class RsrDispParams(ctypes.Structure):
+    _fields_ = [("d_lo", ctypes.c_int32), ("d_hi", ctypes.c_int32), ("lrc_tol", ctypes.c_int32),
+                ("subpixel", ctypes.c_int32)]
+
+
+class RsrRig(ctypes.Structure):
+    _fields_ = [("f", ctypes.c_double), ("baseline", ctypes.c_double), ("u0", ctypes.c_double),
+                ("v0", ctypes.c_double), ("d_min", ctypes.c_double)]
+
+
+class RsrError(RuntimeError):
+    def __init__(self, fn, status):
+        self.status = status
+        super().__init__(f"{fn} failed: status {status} ({strerror(status)})")
+
+
+_lib = None
+P = ctypes.c_void_p
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1807_07433_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        L.rsr_warp.argtypes = [RsrShape, P, P, P, P, P, P]
+        L.rsr_cost_workspace_size.argtypes = [RsrShape]
+        L.rsr_cost_workspace_size.restype = ctypes.c_size_t
+        L.rsr_cost_volume.argtypes = [RsrShape, RsrCostParams, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]
+        L.rsr_aggregate.argtypes = [RsrShape, ctypes.c_int32, RsrAggParams, P, P, P, P, P]
+        L.rsr_disparity.argtypes = [RsrShape, RsrDispParams, P, P, P, P, P, P, P]
+        L.rsr_reconstruct.argtypes = [RsrShape, RsrRig, P, P, P]
+        L.rsr_strerror.argtypes = [ctypes.c_int]
+        L.rsr_strerror.restype = ctypes.c_char_p
+        L.rsr_version.restype = ctypes.c_int
+        for f in ("rsr_warp", "rsr_cost_volume", "rsr_aggregate", "rsr_disparity", "rsr_reconstruct"):
+            getattr(L, f).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def strerror(status: int) -> str:
+    return lib().rsr_strerror(status).decode()
+
+
+def check(fn: str, status: int) -> None:
+    if status != RSR_OK:
+        raise RsrError(fn, status)

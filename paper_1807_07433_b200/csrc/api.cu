@@ -1,0 +1,113 @@
+// C ABI of librsr (include/rsr.h): argument validation, workspace carving and
+// kernel launches.  Validation happens before any launch, so a failing call
+// enqueues nothing (SPEC S:530 convention).
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/rsr.h"
+#include "kernels.h"
+
+namespace {
+
+inline bool shape_ok(const rsr_shape& s) { return s.batch >= 1 && s.height >= 1 && s.width >= 1; }
+inline cudaStream_t as_stream(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+inline int launched(cudaError_t e) { return e == cudaSuccess ? RSR_OK : RSR_E_INTERNAL; }
+inline size_t npix(const rsr_shape& s) { return (size_t)s.batch * s.height * s.width; }
+inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+}  // namespace
+
+extern "C" {
+
+int rsr_version(void) { return 10000; }
+
+const char* rsr_strerror(int status) {
+  switch (status) {
+    case RSR_OK: return "ok";
+    case RSR_E_ARG: return "invalid argument";
+    case RSR_E_DATA: return "data too small for the requested window";
+    case RSR_E_INTERNAL: return "CUDA launch error";
+    default: return "unknown status";
+  }
+}
+
+int rsr_warp(rsr_shape s, const double* alpha_beta, const uint8_t* target, uint8_t* warped,
+             uint8_t* valid, int32_t* shift, void* stream) {
+  if (!shape_ok(s) || !alpha_beta || !target || !warped || !valid || !shift) return RSR_E_ARG;
+  if (s.height > 65535 || s.batch > 65535) return RSR_E_ARG;
+  return launched(rsr::launch_warp(s.batch, s.height, s.width, alpha_beta, target, warped, valid,
+                                   shift, as_stream(stream)));
+}
+
+size_t rsr_cost_workspace_size(rsr_shape s) {
+  if (!shape_ok(s)) return 0;
+  // S_L (int32), inv_L (f32), S_W (int32), inv_W (f32), each [B][H][W]
+  return 4 * align16(sizeof(int32_t) * npix(s));
+}
+
+int rsr_cost_volume(rsr_shape s, rsr_cost_params p, const uint8_t* ref, const uint8_t* warped,
+                    const uint8_t* valid, float* vol_ref, float* vol_tar, uint8_t* nan_ref,
+                    uint8_t* nan_tar, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!shape_ok(s) || !ref || !warped || !valid || !vol_ref || !workspace) return RSR_E_ARG;
+  if (p.rho_block < 1 || p.rho_block > 7 || p.d_hi < p.d_lo) return RSR_E_ARG;
+  const long long D = (long long)p.d_hi - p.d_lo + 1;
+  if (D > 32767) return RSR_E_ARG;
+  if (workspace_bytes < rsr_cost_workspace_size(s)) return RSR_E_ARG;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return RSR_E_ARG;
+  if (s.height < 2 * p.rho_block + 1 || s.width < 2 * p.rho_block + 1) return RSR_E_DATA;
+  if ((size_t)(s.height + 15) / 16 > 65535 || s.batch > 65535) return RSR_E_ARG;
+  const size_t chunk = align16(sizeof(int32_t) * npix(s));
+  char* ws = static_cast<char*>(workspace);
+  int32_t* SL = reinterpret_cast<int32_t*>(ws);
+  float* iL = reinterpret_cast<float*>(ws + chunk);
+  int32_t* SW = reinterpret_cast<int32_t*>(ws + 2 * chunk);
+  float* iW = reinterpret_cast<float*>(ws + 3 * chunk);
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = rsr::launch_block_stats(s.batch, s.height, s.width, p.rho_block, ref, nullptr,
+                                          SL, iL, st);
+  if (e == cudaSuccess)
+    e = rsr::launch_block_stats(s.batch, s.height, s.width, p.rho_block, warped, valid, SW, iW, st);
+  if (e == cudaSuccess)
+    e = rsr::launch_zncc(false, s.batch, s.height, s.width, p.rho_block, p.d_lo, (int)D, ref,
+                         warped, SL, iL, SW, iW, vol_ref, nan_ref, st);
+  if (e == cudaSuccess && vol_tar)
+    e = rsr::launch_zncc(true, s.batch, s.height, s.width, p.rho_block, p.d_lo, (int)D, ref,
+                         warped, SL, iL, SW, iW, vol_tar, nan_tar, st);
+  return launched(e);
+}
+
+int rsr_aggregate(rsr_shape s, int32_t D, rsr_agg_params p, const float* vol, const uint8_t* guide,
+                  const uint8_t* nan_map, float* out, void* stream) {
+  if (!shape_ok(s) || !vol || !guide || !out) return RSR_E_ARG;
+  if (D < 1 || D > 32767 || p.rho < 0 || p.rho > 10) return RSR_E_ARG;
+  if (!(p.gamma_d > 0.f) || std::isinf(p.gamma_d) || !(p.gamma_r > 0.f)) return RSR_E_ARG;
+  if (vol == out) return RSR_E_ARG;
+  if ((s.height + 7) / 8 > 65535) return RSR_E_ARG;
+  const long long nslab = (D + 127) / 128;
+  if ((long long)s.batch * nslab > 65535) return RSR_E_ARG;
+  return launched(rsr::launch_aggregate(s.batch, s.height, s.width, D, p.rho, p.gamma_d, p.gamma_r,
+                                        vol, guide, nan_map, out, as_stream(stream)));
+}
+
+int rsr_disparity(rsr_shape s, rsr_disp_params p, const float* agg_ref, const float* agg_tar,
+                  const int32_t* shift, float* disparity, int16_t* wta_ref, int16_t* wta_tar,
+                  void* stream) {
+  if (!shape_ok(s) || !agg_ref || !agg_tar || !shift || !disparity) return RSR_E_ARG;
+  if (p.d_hi < p.d_lo || (long long)p.d_hi - p.d_lo + 1 > 32767 || p.lrc_tol < 0) return RSR_E_ARG;
+  if (s.width > 32768 || s.height > 65535 || s.batch > 65535) return RSR_E_ARG;
+  const int D = p.d_hi - p.d_lo + 1;
+  return launched(rsr::launch_disparity(s.batch, s.height, s.width, p.d_lo, D, p.lrc_tol,
+                                        p.subpixel != 0, agg_ref, agg_tar, shift, disparity,
+                                        wta_ref, wta_tar, as_stream(stream)));
+}
+
+int rsr_reconstruct(rsr_shape s, rsr_rig rig, const float* disparity, float* xyz, void* stream) {
+  if (!shape_ok(s) || !disparity || !xyz) return RSR_E_ARG;
+  if (!(rig.f > 0) || !(rig.baseline > 0) || !(rig.d_min > 0)) return RSR_E_ARG;
+  if (!std::isfinite(rig.u0) || !std::isfinite(rig.v0) || !std::isfinite(rig.f)) return RSR_E_ARG;
+  return launched(rsr::launch_reconstruct(s.batch, s.height, s.width, rig.f, rig.baseline, rig.u0,
+                                          rig.v0, rig.d_min, disparity, xyz, as_stream(stream)));
+}
+
+}  // extern "C"

@@ -1,0 +1,75 @@
+// Shared device helpers for the rsr kernels (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define RSR_DEVINL __device__ __forceinline__
+
+namespace rsr {
+
+// Packed fp32x2 FMA (SASS FFMA2) with a scalar operand broadcast to both lanes:
+// acc.{x,y} = fma(w, v.{x,y}, acc.{x,y}).  sm_100a only.
+RSR_DEVINL void ffma2_bcast(float2& acc, float w, float2 v) {
+  unsigned long long a, vv, wb;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(a) : "f"(acc.x), "f"(acc.y));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(vv) : "f"(v.x), "f"(v.y));
+  asm("mov.b64 %0, {%1,%1};" : "=l"(wb) : "f"(w));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(wb), "l"(vv));
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(a));
+}
+
+RSR_DEVINL float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+RSR_DEVINL float qnan() { return __int_as_float(0x7fffffff); }
+
+// Clamp to [-1, 1] keeping NaN (fminf/fmaxf would drop it).
+RSR_DEVINL float clamp_unit_keep_nan(float c) {
+  return c > 1.f ? 1.f : (c < -1.f ? -1.f : c);
+}
+
+// ---- mbarrier + 1-D bulk async copy (TMA engine, cp.async.bulk) ----------
+RSR_DEVINL uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+RSR_DEVINL void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+RSR_DEVINL void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+RSR_DEVINL void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// Wait for the mbarrier phase with the given parity.  A bounded spin: a
+// protocol error traps (kernel fails loudly) instead of hanging the GPU.
+RSR_DEVINL void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t spins = 0;; spins++) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (spins > (1u << 24)) __trap();
+  }
+}
+// global -> shared bulk copy completing on `bar` (bytes multiple of 16, 16-B aligned)
+RSR_DEVINL void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace rsr

@@ -1,0 +1,45 @@
+// Internal launch wrappers (C++), one per kernel family.  The public C ABI
+// (include/rsr.h, api.cu) validates arguments and calls these.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rsr {
+
+cudaError_t launch_warp(int B, int H, int W, const double* ab, const uint8_t* target,
+                        uint8_t* warped, uint8_t* valid, int32_t* shift, cudaStream_t st);
+
+// Per-pixel block statistics for the NCC normalisation: S = sum i (int32),
+// inv = 1/sqrt(n*sum i^2 - S^2) (fp32, NaN if the block leaves the image, touches
+// mask==0 or is constant).  mask may be null.
+cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* img,
+                               const uint8_t* mask, int32_t* S, float* inv, cudaStream_t st);
+
+// NCC volume in [B][H][W][D] layout. tar=false: vol[v][u][k] = c(u, v, r);
+// tar=true: vol[v][u'][k] = c(u'+r, v, r).  nan_map optional.
+cudaError_t launch_zncc(bool tar, int B, int H, int W, int rho_b, int d_lo, int D,
+                        const uint8_t* ref, const uint8_t* warped, const int32_t* SL,
+                        const float* invL, const int32_t* SW, const float* invW, float* vol,
+                        uint8_t* nan_map, cudaStream_t st);
+
+cudaError_t launch_aggregate(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r,
+                             const float* vol, const uint8_t* guide, const uint8_t* nan_map,
+                             float* out, cudaStream_t st);
+
+// sliding-window warp-specialised variant (rho <= 7); launch_aggregate dispatches to it
+cudaError_t launch_aggregate_slide(int B, int H, int W, int D, int rho, float gamma_d,
+                                   float gamma_r, const float* vol, const uint8_t* guide,
+                                   const uint8_t* nan_map, float* out, cudaStream_t st);
+size_t aggregate_slide_smem(int D, int rho, int H);
+size_t aggregate_tiled_smem(int D, int rho);
+
+cudaError_t launch_disparity(int B, int H, int W, int d_lo, int D, int tol, int subpix,
+                             const float* agg_ref, const float* agg_tar, const int32_t* shift,
+                             float* disp, int16_t* wta_ref, int16_t* wta_tar, cudaStream_t st);
+
+cudaError_t launch_reconstruct(int B, int H, int W, double f, double baseline, double u0,
+                               double v0, double d_min, const float* disp, float* xyz,
+                               cudaStream_t st);
+
+}  // namespace rsr

@@ -1,0 +1,372 @@
+// K2 — NCC cost volumes (Eqs. (3)-(5)).
+//
+// c(u,v,r) = (n S_lw - S_l S_w) / (sqrt(n S_ll - S_l^2) sqrt(n S_ww - S_w^2)),
+// the integer-sum form of Eq. (3) with Eqs. (4)-(5) (multiply numerator and
+// denominator of Eq. (3) by n).  As P:106 prescribes, the block statistics
+// (mu, sigma) are computed once per pixel ("pre-calculated and stored") by
+// k_block_stats, and only the dot product S_lw is per-disparity work.
+//
+// k_zncc keeps S_lw exact: every product i_l * i_w <= 65025 and every partial
+// sum of at most 225 of them is an integer below 2^24, so fp32 FFMA arithmetic
+// is exact.  Each thread owns X=4 columns x R=8 disparities and slides the
+// vertical sums V(x, r) = sum_dy F(y+dy, x) G(y+dy, x -/+ r) down a band of
+// BY=16 rows (two FFMAs per (x, r) per row), then forms the horizontal
+// (2p+1)-sums in registers.  The numerator n*S_lw - S_l*S_w is evaluated with
+// an error-free product split (fmaf remainder) so catastrophic cancellation
+// cannot lose the result; one fp32 normalisation per entry remains, which is
+// the only difference from the fp64 oracle (|dc| ~ 1e-7).
+//
+// Output layout [B][H][W][D]: the thread's 8 disparities of one pixel are 32
+// contiguous bytes (two 16-byte stores); 8 lanes cover one pixel's 64 k.
+#include <cstdio>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rsr {
+
+// ---------------------------------------------------------------------------
+// Block statistics: S = sum i, inv = 1/sqrt(n*sum i^2 - S^2) over the
+// (2p+1)^2 block centred at each pixel; inv = NaN if the block leaves the
+// image, holds mask == 0 (warp-invalid, reading 7) or is constant
+// (exact integer test, reading 6).
+// ---------------------------------------------------------------------------
+constexpr int ST_TX = 64, ST_TY = 16;
+
+__global__ void __launch_bounds__(256) k_block_stats(int H, int W, int p,
+                                                     const uint8_t* __restrict__ img,
+                                                     const uint8_t* __restrict__ mask,
+                                                     int32_t* __restrict__ Sout,
+                                                     float* __restrict__ inv) {
+  extern __shared__ int st_smem[];
+  const int TC = ST_TX + 2 * p, TR = ST_TY + 2 * p;
+  int* pix = st_smem;                // [TR][TC] value
+  int* msk = pix + TR * TC;          // [TR][TC] mask (1 inside image and valid)
+  int* cS = msk + TR * TC;           // [ST_TY][TC] vertical sums
+  int* cSS = cS + ST_TY * TC;
+  int* cM = cSS + ST_TY * TC;
+  const int b = blockIdx.z, x0 = blockIdx.x * ST_TX, y0 = blockIdx.y * ST_TY;
+  const size_t base = (size_t)b * H * W;
+  for (int i = threadIdx.x; i < TR * TC; i += blockDim.x) {
+    const int yy = y0 - p + i / TC, xx = x0 - p + i % TC;
+    const bool in = yy >= 0 && yy < H && xx >= 0 && xx < W;
+    const size_t g = base + (size_t)yy * W + xx;
+    pix[i] = in ? (int)img[g] : 0;
+    msk[i] = in ? (mask ? (int)(mask[g] != 0) : 1) : 0;
+  }
+  __syncthreads();
+  // vertical sliding sums, one column per thread
+  for (int c = threadIdx.x; c < TC; c += blockDim.x) {
+    int s = 0, ss = 0, m = 0;
+    for (int r = 0; r < 2 * p + 1; r++) {
+      const int v = pix[r * TC + c];
+      s += v; ss += v * v; m += msk[r * TC + c];
+    }
+    for (int y = 0; y < ST_TY; y++) {
+      cS[y * TC + c] = s; cSS[y * TC + c] = ss; cM[y * TC + c] = m;
+      if (y + 1 < ST_TY) {
+        const int vin = pix[(y + 2 * p + 1) * TC + c], vout = pix[y * TC + c];
+        s += vin - vout; ss += vin * vin - vout * vout;
+        m += msk[(y + 2 * p + 1) * TC + c] - msk[y * TC + c];
+      }
+    }
+  }
+  __syncthreads();
+  // horizontal sliding sums over chunks of 16 columns
+  const int n = (2 * p + 1) * (2 * p + 1);
+  for (int it = threadIdx.x; it < ST_TY * (ST_TX / 16); it += blockDim.x) {
+    const int y = it / (ST_TX / 16), xc = (it % (ST_TX / 16)) * 16;
+    int s = 0, ss = 0, m = 0;
+    for (int d = 0; d < 2 * p + 1; d++) {
+      s += cS[y * TC + xc + d]; ss += cSS[y * TC + xc + d]; m += cM[y * TC + xc + d];
+    }
+    const int yy = y0 + y;
+    for (int i = 0; i < 16; i++) {
+      const int xx = x0 + xc + i;
+      if (yy < H && xx < W) {
+        const bool inside = yy >= p && yy <= H - 1 - p && xx >= p && xx <= W - 1 - p;
+        const long long var = (long long)n * ss - (long long)s * s;
+        const bool ok = inside && m == n && var != 0;
+        const size_t g = base + (size_t)yy * W + xx;
+        Sout[g] = s;
+        inv[g] = ok ? (float)(1.0 / sqrt((double)var)) : qnan();
+      }
+      if (i + 1 < 16) {
+        const int a = y * TC + xc + i + 2 * p + 1, o = y * TC + xc + i;
+        s += cS[a] - cS[o]; ss += cSS[a] - cSS[o]; m += cM[a] - cM[o];
+      }
+    }
+  }
+}
+
+cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* img,
+                               const uint8_t* mask, int32_t* S, float* inv, cudaStream_t st) {
+  const int p = rho_b;
+  const int TC = ST_TX + 2 * p, TR = ST_TY + 2 * p;
+  const size_t smem = sizeof(int) * (size_t)(2 * TR * TC + 3 * ST_TY * TC);
+  dim3 grid((W + ST_TX - 1) / ST_TX, (H + ST_TY - 1) / ST_TY, B);
+  k_block_stats<<<grid, 256, smem, st>>>(H, W, p, img, mask, S, inv);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// NCC volume kernel
+// ---------------------------------------------------------------------------
+constexpr int ZX = 4;     // columns per thread
+constexpr int ZR = 8;     // disparities per thread
+constexpr int ZTX = 64;   // columns per CTA (16 column groups)
+constexpr int ZBY = 16;   // rows per CTA (vertical sliding band)
+
+struct ZnccGeom {
+  int FC, GC, SGC, gpad, NR;
+};
+
+__host__ __device__ inline ZnccGeom zncc_geom(int p, int D) {
+  ZnccGeom g;
+  g.NR = ZBY + 2 * p;
+  g.FC = ((ZTX + 2 * p + 3) / 4) * 4 + 4;
+  g.gpad = (4 - (D & 3)) & 3;
+  g.GC = ((ZTX + 2 * p + D - 1 + g.gpad + 3) / 4) * 4 + 8;
+  g.SGC = ((ZTX + D - 1 + g.gpad + 3) / 4) * 4 + 8;
+  return g;
+}
+
+template <int P, bool TAR>
+__global__ void __launch_bounds__(256) k_zncc(int H, int W, int d_lo, int D, int Dst, int koff,
+                                              bool nan_accumulate,
+                                              const uint8_t* __restrict__ ref,
+                                              const uint8_t* __restrict__ warped,
+                                              const int32_t* __restrict__ SLg,
+                                              const float* __restrict__ invLg,
+                                              const int32_t* __restrict__ SWg,
+                                              const float* __restrict__ invWg,
+                                              float* __restrict__ vol,
+                                              uint8_t* __restrict__ nan_map) {
+  constexpr int NJ = ZX + 2 * P;          // V columns per thread
+  constexpr int NG = ZX + 2 * P + ZR - 1; // G run length
+  constexpr int NF4 = (NJ + 3) / 4, NG4 = (NG + 3) / 4;
+  constexpr int SGR = ZX + ZR - 1;        // G-stats run length
+  constexpr int NS4 = (SGR + 3) / 4;
+  const ZnccGeom gm = zncc_geom(P, D);
+  extern __shared__ __align__(16) float zsm[];
+  float* Fs = zsm;                          // [NR][FC]
+  float* Gs = Fs + gm.NR * gm.FC;           // [NR][GC]
+  float* sFs = Gs + gm.NR * gm.GC;          // [ZBY][ZTX]
+  float* iFs = sFs + ZBY * ZTX;             // [ZBY][ZTX]
+  float* sGs = iFs + ZBY * ZTX;             // [ZBY][SGC]
+  float* iGs = sGs + ZBY * gm.SGC;          // [ZBY][SGC]
+  int* flags = reinterpret_cast<int*>(iGs + ZBY * gm.SGC);  // [ZBY][ZTX]
+
+  const int b = blockIdx.z, x0 = blockIdx.x * ZTX, y0 = blockIdx.y * ZBY;
+  const int d_hi = d_lo + D - 1;
+  const size_t ibase = (size_t)b * H * W;
+  // F = image at the fixed column; G = image at the shifted column x + sg*r.
+  const uint8_t* Fimg = TAR ? warped : ref;
+  const uint8_t* Gimg = TAR ? ref : warped;
+  const int32_t* SFg = TAR ? SWg : SLg;
+  const float* iFg = TAR ? invWg : invLg;
+  const int32_t* SGg = TAR ? SLg : SWg;
+  const float* iGg = TAR ? invLg : invWg;
+  // first image column held in Gs / sGs
+  const int g0 = TAR ? (x0 - P + d_lo) : (x0 - P - d_hi - gm.gpad);
+  const int s0 = TAR ? (x0 + d_lo) : (x0 - d_hi - gm.gpad);
+
+  for (int i = threadIdx.x; i < gm.NR * gm.FC; i += blockDim.x) {
+    const int yy = y0 - P + i / gm.FC, xx = x0 - P + i % gm.FC;
+    Fs[i] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? (float)Fimg[ibase + (size_t)yy * W + xx] : 0.f;
+  }
+  for (int i = threadIdx.x; i < gm.NR * gm.GC; i += blockDim.x) {
+    const int yy = y0 - P + i / gm.GC, xx = g0 + i % gm.GC;
+    Gs[i] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? (float)Gimg[ibase + (size_t)yy * W + xx] : 0.f;
+  }
+  for (int i = threadIdx.x; i < ZBY * ZTX; i += blockDim.x) {
+    const int yy = y0 + i / ZTX, xx = x0 + i % ZTX;
+    const bool in = yy < H && xx < W;
+    sFs[i] = in ? (float)SFg[ibase + (size_t)yy * W + xx] : 0.f;
+    iFs[i] = in ? iFg[ibase + (size_t)yy * W + xx] : qnan();
+    flags[i] = 0;
+  }
+  for (int i = threadIdx.x; i < ZBY * gm.SGC; i += blockDim.x) {
+    const int yy = y0 + i / gm.SGC, xx = s0 + i % gm.SGC;
+    const bool in = yy < H && xx >= 0 && xx < W;
+    sGs[i] = in ? (float)SGg[ibase + (size_t)yy * W + xx] : 0.f;
+    iGs[i] = in ? iGg[ibase + (size_t)yy * W + xx] : qnan();
+  }
+  __syncthreads();
+
+  const int n_rg = (D + ZR - 1) / ZR;
+  const int rg = threadIdx.x % n_rg, cg = threadIdx.x / n_rg;
+  if (cg >= ZTX / ZX) return;
+  const int r0 = d_lo + ZR * rg;               // first residual disparity of the thread
+  const int u_t = x0 + ZX * cg;                // first column of the thread
+  // run starts (element index in the smem row)
+  const int f_start = ZX * cg;                                  // column u_t - P
+  const int g_start = TAR ? (ZX * cg + ZR * rg)                 // column u_t - P + r0
+                          : (ZX * cg + D - ZR - ZR * rg + gm.gpad);  // column u_t - P - r0 - 7
+  const int sg_start = TAR ? (ZX * cg + ZR * rg) : (ZX * cg + D - ZR - ZR * rg + gm.gpad);
+  const float nf = (float)((2 * P + 1) * (2 * P + 1));
+
+  float V[NJ][ZR];
+#pragma unroll
+  for (int j = 0; j < NJ; j++)
+#pragma unroll
+    for (int q = 0; q < ZR; q++) V[j][q] = 0.f;
+
+  auto accumulate_row = [&](int srow, float sign) {
+    float f[NF4 * 4], g[NG4 * 4];
+    const float4* fr = reinterpret_cast<const float4*>(Fs + srow * gm.FC + f_start);
+    const float4* gr = reinterpret_cast<const float4*>(Gs + srow * gm.GC + g_start);
+#pragma unroll
+    for (int i = 0; i < NF4; i++) {
+      const float4 t = fr[i];
+      f[4 * i] = t.x; f[4 * i + 1] = t.y; f[4 * i + 2] = t.z; f[4 * i + 3] = t.w;
+    }
+#pragma unroll
+    for (int i = 0; i < NG4; i++) {
+      const float4 t = gr[i];
+      g[4 * i] = t.x; g[4 * i + 1] = t.y; g[4 * i + 2] = t.z; g[4 * i + 3] = t.w;
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; j++) {
+      const float fj = sign * f[j];
+#pragma unroll
+      for (int q = 0; q < ZR; q++) {
+        const int m = TAR ? (j + q) : (j - q + ZR - 1);
+        V[j][q] = fmaf(fj, g[m], V[j][q]);
+      }
+    }
+  };
+
+  const int nrows = min(ZBY, H - y0);
+  for (int y = 0; y < nrows; y++) {
+    if (y == 0) {
+#pragma unroll 1
+      for (int dy = 0; dy < 2 * P + 1; dy++) accumulate_row(dy, 1.f);
+    } else {
+      accumulate_row(y + 2 * P, 1.f);
+      accumulate_row(y - 1, -1.f);
+    }
+    // block statistics of this row
+    float sF[ZX], iF[ZX], sG[NS4 * 4], iG[NS4 * 4];
+    {
+      const float4 a = *reinterpret_cast<const float4*>(sFs + y * ZTX + ZX * cg);
+      const float4 c = *reinterpret_cast<const float4*>(iFs + y * ZTX + ZX * cg);
+      sF[0] = a.x; sF[1] = a.y; sF[2] = a.z; sF[3] = a.w;
+      iF[0] = c.x; iF[1] = c.y; iF[2] = c.z; iF[3] = c.w;
+      const float4* sr = reinterpret_cast<const float4*>(sGs + y * gm.SGC + sg_start);
+      const float4* ir = reinterpret_cast<const float4*>(iGs + y * gm.SGC + sg_start);
+#pragma unroll
+      for (int i = 0; i < NS4; i++) {
+        const float4 t = sr[i], u = ir[i];
+        sG[4 * i] = t.x; sG[4 * i + 1] = t.y; sG[4 * i + 2] = t.z; sG[4 * i + 3] = t.w;
+        iG[4 * i] = u.x; iG[4 * i + 1] = u.y; iG[4 * i + 2] = u.z; iG[4 * i + 3] = u.w;
+      }
+    }
+    const int yy = y0 + y;
+    float* vrow = vol + ((ibase + (size_t)yy * W) * Dst) + koff;
+#pragma unroll
+    for (int i = 0; i < ZX; i++) {
+      const int u = u_t + i;
+      float out[ZR];
+      bool anynan = false, anyfin = false;
+#pragma unroll
+      for (int q = 0; q < ZR; q++) {
+        float s = 0.f;
+#pragma unroll
+        for (int dx = 0; dx < 2 * P + 1; dx++) s += V[i + dx][q];
+        const int m = TAR ? (i + q) : (i - q + ZR - 1);
+        // left block = L at u_left, right block = W at u_left - r
+        const float sL = TAR ? sG[m] : sF[i];
+        const float sR = TAR ? sF[i] : sG[m];
+        const float iL = TAR ? iG[m] : iF[i];
+        const float iR = TAR ? iF[i] : iG[m];
+        const float a = nf * s;
+        const float ae = fmaf(nf, s, -a);
+        const float bb = sL * sR;
+        const float be = fmaf(sL, sR, -bb);
+        const float num = (a - bb) + (ae - be);
+        const float c = clamp_unit_keep_nan((num * iL) * iR);
+        out[q] = c;
+        anynan |= (r0 + q <= d_hi) && (c != c);
+        anyfin |= (r0 + q <= d_hi) && (c == c);
+      }
+      if (u < W) {
+        float* dst = vrow + (size_t)u * Dst + (r0 - d_lo);
+        if ((Dst & 3) == 0 && (koff & 3) == 0 && r0 + ZR - 1 <= d_hi) {
+          reinterpret_cast<float4*>(dst)[0] = make_float4(out[0], out[1], out[2], out[3]);
+          reinterpret_cast<float4*>(dst)[1] = make_float4(out[4], out[5], out[6], out[7]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < ZR; q++)
+            if (r0 + q <= d_hi) dst[q] = out[q];
+        }
+        const int fl = (anynan ? 1 : 0) | (anyfin ? 2 : 0);
+        if (fl && nan_map) atomicOr(&flags[y * ZTX + ZX * cg + i], fl);
+      }
+    }
+  }
+  if (nan_map) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < ZBY * ZTX; i += blockDim.x) {
+      const int yy = y0 + i / ZTX, xx = x0 + i % ZTX;
+      if (yy < H && xx < W) {
+        uint8_t* m = nan_map + ibase + (size_t)yy * W + xx;
+        *m = (uint8_t)(flags[i] | (nan_accumulate ? *m : 0));
+      }
+    }
+  }
+}
+
+template <int P, bool TAR>
+static cudaError_t zncc_launch_t(int B, int H, int W, int d_lo, int D, int Dst, int koff,
+                                 bool nan_acc, const uint8_t* ref,
+                                 const uint8_t* warped, const int32_t* SL, const float* invL,
+                                 const int32_t* SW, const float* invW, float* vol,
+                                 uint8_t* nan_map, cudaStream_t st) {
+  const ZnccGeom gm = zncc_geom(P, D);
+  const size_t smem = sizeof(float) * ((size_t)gm.NR * gm.FC + (size_t)gm.NR * gm.GC +
+                                       2 * ZBY * ZTX + 2 * (size_t)ZBY * gm.SGC) +
+                      sizeof(int) * ZBY * ZTX;
+  auto kern = k_zncc<P, TAR>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) { cudaGetLastError(); return e; }
+  const int n_rg = (D + ZR - 1) / ZR;
+  const int threads = n_rg * (ZTX / ZX);
+  // threads > 1024 is rejected by the API (D > 512 would need a k-slab split)
+  dim3 grid((W + ZTX - 1) / ZTX, (H + ZBY - 1) / ZBY, B);
+  kern<<<grid, threads, smem, st>>>(H, W, d_lo, D, Dst, koff, nan_acc, ref, warped, SL, invL, SW,
+                                    invW, vol, nan_map);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zncc(bool tar, int B, int H, int W, int rho_b, int d_lo, int D,
+                        const uint8_t* ref, const uint8_t* warped, const int32_t* SL,
+                        const float* invL, const int32_t* SW, const float* invW, float* vol,
+                        uint8_t* nan_map, cudaStream_t st) {
+  // Disparity slabs of at most 128 (<= 256 threads per CTA); later slabs OR
+  // their NaN flags into the map written by the first.
+  constexpr int SLAB = 128;
+  for (int k0 = 0; k0 < D; k0 += SLAB) {
+    const int Ds = D - k0 < SLAB ? D - k0 : SLAB;
+    const int dl = d_lo + k0;
+    const bool acc = k0 > 0;
+    cudaError_t e;
+#define RSR_Z(PP)                                                                                \
+  case PP:                                                                                       \
+    e = tar ? zncc_launch_t<PP, true>(B, H, W, dl, Ds, D, k0, acc, ref, warped, SL, invL, SW,     \
+                                      invW, vol, nan_map, st)                                    \
+            : zncc_launch_t<PP, false>(B, H, W, dl, Ds, D, k0, acc, ref, warped, SL, invL, SW,    \
+                                       invW, vol, nan_map, st);                                  \
+    break;
+    switch (rho_b) {
+      RSR_Z(1) RSR_Z(2) RSR_Z(3) RSR_Z(4) RSR_Z(5) RSR_Z(6) RSR_Z(7)
+      default:
+        return cudaErrorInvalidValue;
+    }
+#undef RSR_Z
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace rsr

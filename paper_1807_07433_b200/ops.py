@@ -1,0 +1,140 @@
+"""Python-level names of the five C-ABI calls (include/rsr.h), over torch CUDA
+tensors.  Each function checks dtype / device / shape / contiguity, allocates
+missing outputs with torch (device memory plumbing) and calls the library on
+the current torch CUDA stream.  No arithmetic of the method happens here."""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from ._lib import (RsrAggParams, RsrCostParams, RsrDispParams, RsrRig, RsrShape, check, lib)
+
+
+def _ptr(t):
+    return None if t is None else ctypes_ptr(t)
+
+
+def ctypes_ptr(t: torch.Tensor):
+    if not t.is_cuda:
+        raise ValueError("rsr: tensors must live on a CUDA device (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError("rsr: tensors must be contiguous")
+    return t.data_ptr()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _expect(t, dtype, shape, name):
+    if t.dtype != dtype:
+        raise TypeError(f"rsr: {name} must be {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"rsr: {name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+
+
+def _bhw(img: torch.Tensor):
+    if img.dim() == 2:
+        img = img.unsqueeze(0)
+    if img.dim() != 3:
+        raise ValueError("rsr: images must be [B,H,W] or [H,W]")
+    return img, RsrShape(*img.shape)
+
+
+def rsr_warp(target, alpha_beta, warped=None, valid=None, shift=None):
+    """Step 1: returns (warped uint8 [B,H,W], valid uint8 [B,H,W], shift int32 [B,H])."""
+    target, s = _bhw(target)
+    B, H, W = target.shape
+    _expect(target, torch.uint8, (B, H, W), "target")
+    alpha_beta = alpha_beta.reshape(B, 2)
+    _expect(alpha_beta, torch.float64, (B, 2), "alpha_beta")
+    warped = torch.empty_like(target) if warped is None else warped
+    valid = torch.empty_like(target) if valid is None else valid
+    shift = torch.empty((B, H), dtype=torch.int32, device=target.device) if shift is None else shift
+    check("rsr_warp", lib().rsr_warp(s, _ptr(alpha_beta), _ptr(target), _ptr(warped), _ptr(valid),
+                                     _ptr(shift), _stream()))
+    return warped, valid, shift
+
+
+def cost_workspace_bytes(B, H, W) -> int:
+    return int(lib().rsr_cost_workspace_size(RsrShape(B, H, W)))
+
+
+def rsr_cost_volume(ref, warped, valid, rho_block, d_lo, d_hi, *, with_tar=True, with_nan_maps=True,
+                    vol_ref=None, vol_tar=None, nan_ref=None, nan_tar=None, workspace=None):
+    """Step 2 (Eqs. 3-5): returns (vol_ref, vol_tar|None, nan_ref|None, nan_tar|None),
+    volumes float32 [B,H,W,D]."""
+    ref, s = _bhw(ref)
+    B, H, W = ref.shape
+    warped, _ = _bhw(warped)
+    valid, _ = _bhw(valid)
+    D = d_hi - d_lo + 1
+    dev = ref.device
+    if vol_ref is None:
+        vol_ref = torch.empty((B, H, W, D), dtype=torch.float32, device=dev)
+    if with_tar and vol_tar is None:
+        vol_tar = torch.empty((B, H, W, D), dtype=torch.float32, device=dev)
+    if with_nan_maps:
+        nan_ref = torch.empty((B, H, W), dtype=torch.uint8, device=dev) if nan_ref is None else nan_ref
+        if with_tar and nan_tar is None:
+            nan_tar = torch.empty((B, H, W), dtype=torch.uint8, device=dev)
+    nbytes = cost_workspace_bytes(B, H, W)
+    if workspace is None:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    check("rsr_cost_volume", lib().rsr_cost_volume(
+        s, RsrCostParams(rho_block, d_lo, d_hi), _ptr(ref), _ptr(warped), _ptr(valid), _ptr(vol_ref),
+        _ptr(vol_tar), _ptr(nan_ref), _ptr(nan_tar), _ptr(workspace), workspace.numel(), _stream()))
+    return vol_ref, vol_tar, nan_ref, nan_tar
+
+
+def rsr_aggregate(vol, guide, rho, gamma_d, gamma_r, nan_map=None, out=None):
+    """Step 3 (Eqs. 8-10): aggregated volume float32 [B,H,W,D]."""
+    guide, s = _bhw(guide)
+    B, H, W = guide.shape
+    if vol.dim() == 3:
+        vol = vol.unsqueeze(0)
+    D = vol.shape[-1]
+    _expect(vol, torch.float32, (B, H, W, D), "vol")
+    out = torch.empty_like(vol) if out is None else out
+    if nan_map is not None:
+        nan_map, _ = _bhw(nan_map)
+    check("rsr_aggregate", lib().rsr_aggregate(
+        s, D, RsrAggParams(rho, float(gamma_d), float(gamma_r)), _ptr(vol), _ptr(guide),
+        _ptr(nan_map), _ptr(out), _stream()))
+    return out
+
+
+def rsr_disparity(agg_ref, agg_tar, shift, d_lo, d_hi, lrc_tol, subpixel=True, disparity=None,
+                  wta_ref=None, wta_tar=None, with_wta=False):
+    """Steps 4-5 (Eqs. 11-12): returns (disparity f32 [B,H,W], wta_ref, wta_tar)."""
+    if agg_ref.dim() == 3:
+        agg_ref, agg_tar = agg_ref.unsqueeze(0), agg_tar.unsqueeze(0)
+    B, H, W, D = agg_ref.shape
+    shift = shift.reshape(B, H)
+    _expect(shift, torch.int32, (B, H), "shift")
+    dev = agg_ref.device
+    disparity = torch.empty((B, H, W), dtype=torch.float32, device=dev) if disparity is None else disparity
+    if with_wta:
+        wta_ref = torch.empty((B, H, W), dtype=torch.int16, device=dev) if wta_ref is None else wta_ref
+        wta_tar = torch.empty((B, H, W), dtype=torch.int16, device=dev) if wta_tar is None else wta_tar
+    check("rsr_disparity", lib().rsr_disparity(
+        RsrShape(B, H, W), RsrDispParams(d_lo, d_hi, lrc_tol, 1 if subpixel else 0), _ptr(agg_ref),
+        _ptr(agg_tar), _ptr(shift), _ptr(disparity), _ptr(wta_ref), _ptr(wta_tar), _stream()))
+    return disparity, wta_ref, wta_tar
+
+
+def rsr_reconstruct(disparity, f, baseline, u0=None, v0=None, d_min=1.0, xyz=None):
+    """Step 5b: points float32 [B,H,W,3]; u0/v0 default to the image centre."""
+    if disparity.dim() == 2:
+        disparity = disparity.unsqueeze(0)
+    B, H, W = disparity.shape
+    u0 = (W - 1) / 2.0 if u0 is None else u0
+    v0 = (H - 1) / 2.0 if v0 is None else v0
+    xyz = torch.empty((B, H, W, 3), dtype=torch.float32, device=disparity.device) if xyz is None else xyz
+    check("rsr_reconstruct", lib().rsr_reconstruct(
+        RsrShape(B, H, W), RsrRig(f, baseline, u0, v0, d_min), _ptr(disparity), _ptr(xyz), _stream()))
+    return xyz
+
+
+_ = math  # (kept for callers that pass math.inf for gamma_r)

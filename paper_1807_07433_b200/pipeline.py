@@ -1,0 +1,79 @@
+"""Buffer plumbing for the whole hot path: allocate every device buffer once
+(torch), then enqueue the five C-ABI calls in the paper's order on the current
+stream.  No arithmetic of the method happens here."""
+from __future__ import annotations
+
+import dataclasses
+
+import torch
+
+from . import ops
+
+
+@dataclasses.dataclass(frozen=True)
+class StereoParams:
+    d_lo: int
+    d_hi: int
+    rho_block: int
+    rho_agg: int
+    gamma_d: float
+    gamma_r: float
+    lrc_tol: int = 1
+    subpixel: bool = True
+    focal: float = 700.0
+    baseline: float = 0.12
+    d_min: float = 1.0
+
+    @property
+    def D(self):
+        return self.d_hi - self.d_lo + 1
+
+    @staticmethod
+    def from_config(cfg):
+        return StereoParams(cfg.d_lo, cfg.d_hi, cfg.rho_block, cfg.rho_agg, cfg.gamma_d, cfg.gamma_r,
+                            cfg.lrc_tol, True, cfg.focal, cfg.baseline)
+
+
+class StereoPipeline:
+    """Pre-allocated buffers for a [B,H,W] batch; run() enqueues the whole path.
+
+    Launches per run(): warp 1, cost volume 4 (2 block-stats, ref and tar
+    volumes), aggregation 2, disparity 1, reconstruction 1.
+    """
+
+    LAUNCHES_PER_RUN = 9
+
+    def __init__(self, B, H, W, params: StereoParams, device="cuda"):
+        self.B, self.H, self.W, self.p = B, H, W, params
+        D = params.D
+        dev = torch.device(device)
+        e = lambda shape, dt: torch.empty(shape, dtype=dt, device=dev)  # noqa: E731
+        self.warped = e((B, H, W), torch.uint8)
+        self.valid = e((B, H, W), torch.uint8)
+        self.shift = e((B, H), torch.int32)
+        self.vol_ref = e((B, H, W, D), torch.float32)
+        self.vol_tar = e((B, H, W, D), torch.float32)
+        self.nan_ref = e((B, H, W), torch.uint8)
+        self.nan_tar = e((B, H, W), torch.uint8)
+        self.agg_ref = e((B, H, W, D), torch.float32)
+        self.agg_tar = e((B, H, W, D), torch.float32)
+        self.disparity = e((B, H, W), torch.float32)
+        self.wta_ref = e((B, H, W), torch.int16)
+        self.wta_tar = e((B, H, W), torch.int16)
+        self.xyz = e((B, H, W, 3), torch.float32)
+        self.workspace = e((ops.cost_workspace_bytes(B, H, W),), torch.uint8)
+
+    def run(self, left, right, alpha_beta, with_wta=True):
+        p = self.p
+        ops.rsr_warp(right, alpha_beta, self.warped, self.valid, self.shift)
+        ops.rsr_cost_volume(left, self.warped, self.valid, p.rho_block, p.d_lo, p.d_hi,
+                            vol_ref=self.vol_ref, vol_tar=self.vol_tar, nan_ref=self.nan_ref,
+                            nan_tar=self.nan_tar, workspace=self.workspace)
+        ops.rsr_aggregate(self.vol_ref, left, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_ref, self.agg_ref)
+        ops.rsr_aggregate(self.vol_tar, self.warped, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_tar,
+                          self.agg_tar)
+        ops.rsr_disparity(self.agg_ref, self.agg_tar, self.shift, p.d_lo, p.d_hi, p.lrc_tol, p.subpixel,
+                          self.disparity, self.wta_ref if with_wta else None,
+                          self.wta_tar if with_wta else None)
+        ops.rsr_reconstruct(self.disparity, p.focal, p.baseline, d_min=p.d_min, xyz=self.xyz)
+        return self.disparity
