@@ -36,7 +36,7 @@ def log(*a):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=8, help="frames per rank per step")
     ap.add_argument("--pool", type=int, default=16, help="distinct input frames per rank")
@@ -94,7 +94,7 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
@@ -168,6 +168,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_1807_07433_b200 as rsr
+    from paper_1807_07433_b200 import dist as rdist
 
     assert torch.cuda.is_available(), "bench.py needs a CUDA device"
     torch.cuda.set_device(local)
@@ -181,7 +182,7 @@ def main():
 
     # ---- inputs: a pool of distinct seeded frames per rank, resident in HBM ----
     pool = args.pool
-    idx = [rank * pool + i for i in range(pool)]
+    idx = list(rdist.shard(pool * world, rank, world))   # this rank's frames of the c5 stream
     left_np, right_np, ab_np = synth.make_batch(cfg, idx)
     left = torch.from_numpy(left_np).to(dev)
     right = torch.from_numpy(right_np).to(dev)
@@ -223,7 +224,7 @@ def main():
             e = torch.cuda.Event(enable_timing=True); e.record(stream); ev["disp1"].append(e)
         rsr.rsr_reconstruct(pipe.disparity, p.focal, p.baseline, d_min=p.d_min, xyz=pipe.xyz)
         if world > 1 and not args.no_gather:
-            dist.gather(pipe.disparity, gather_list, dst=0)
+            rdist.gather_maps(pipe.disparity, dst=0, out=gather_list)
 
     launches_per_step = 1 + 2 + 2 * ((cfg.D + 127) // 128) + 2 + 1 + 1
 
@@ -245,11 +246,7 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = rdist.max_over_ranks(t0.elapsed_time(t1), dev)
 
     def avg_ms(a, b):
         return statistics.mean(x.elapsed_time(y) for x, y in zip(ev[a], ev[b]))
@@ -288,11 +285,7 @@ def main():
             e2e_step()
         a1.record(stream)
         torch.cuda.synchronize()
-        ems = a0.elapsed_time(a1)
-        if world > 1:
-            t = torch.tensor([ems], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = rdist.max_over_ranks(a0.elapsed_time(a1), dev)
         e2e = {"value": frames / (ems / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": int(hl.numel() + hr.numel() + hab.numel() * 8),
                "d2h_bytes_per_step": int(hout.numel() * 4)}
