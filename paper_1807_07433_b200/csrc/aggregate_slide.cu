@@ -1,27 +1,41 @@
-// K3 (sliding-window, warp-specialised) — bilateral cost aggregation,
-// PAPER.md:128-152, Eq. (8) with Eqs. (9)-(10); same definition and readings
-// as aggregate.cu (readings 10-12).  Used for rho <= 7.
+// K3 — bilateral cost aggregation (fast bilateral stereo), PAPER.md:128-152,
+// Eq. (8) with the weights of Eqs. (9)-(10):
+//   A(u,v,k) = sum_t w_t C(u+dx, v+dy, k) / sum_t w_t,
+//   w_t = exp(-(dx^2+dy^2)/gamma_d^2) * exp(-(g(u+dx,v+dy) - g(u,v))^2/gamma_r^2),
+// taps outside the image or with a NaN cost skipped, NaN iff the centre cost is
+// NaN (readings 10-12).  Used for rho <= 7; the paper's bottleneck
+// (P:154), FP32-FMA bound: 2 (2 rho + 1)^2 flop per output.
 //
-// Why this shape (profiles/r01_*):
-//  * A CTA owns a 32-column strip and a chunk of R output rows and slides
-//    down it one input row at a time.  A consumer thread holds the 2 rho + 1
-//    output rows whose windows contain the current input row ("ages" 0..2rho)
-//    x 8 disparities as 4 packed pairs, so every input row feeds every held
-//    row: no predicated-off FMA at tile edges.  The register slot of an age
-//    rotates by one per input row; the loop is unrolled by the period
-//    2 rho + 1 so all register indices are static.
-//  * Producer warps (4) compute the weights of the next input rows once per
-//    CTA (exp2 on the MUFU pipe), write them in age order to a weight stage,
-//    keep the per-pixel sum of weights, and drive the cost-row pipeline
-//    (one 256-byte cp.async.bulk per pixel column, TMA engine).  Consumers and
-//    producers hand off through mbarriers: no CTA-wide barrier in the loop.
-//  * Inner product: FFMA2 (fma.rn.f32x2) with the tap weight as scalar
-//    broadcast operand; per tap a consumer loads 2 x LDS.128 of costs and
-//    4 x LDS.128 of weights for 52 FFMA2 (104 FMA).
-//  * Clean chunks (footprint inside the image and NaN-free per nan_map) use
-//    pair = (k, k+1) and a per-pixel denominator; other chunks use
-//    pair = (C0, V) (cost or 0, validity) in two passes, exact for any NaN
-//    pattern.
+// Design ("k-lane sliding window", DESIGN.md §6 K3):
+//  * Lanes run along the disparity axis.  A group of G = KS/8 lanes owns one
+//    output column x of a 32-column strip; lane l holds disparities
+//    {4l..4l+3} and {4G+4l..4G+4l+3} of the slab.  The bilateral weight w(p,t)
+//    does not depend on k, so all lanes of a group read the SAME weight
+//    address: one LDS.128 broadcast serves 4 weights to 4 groups (one
+//    shared-memory wavefront), each weight feeding 64 FMAs.  Cost loads are
+//    per lane and contiguous (8 lanes x 16 B = one 128-B row per group).
+//  * The strip slides down one input row at a time.  A thread keeps the
+//    2 rho + 1 output rows whose windows contain the current input row
+//    ("ages") x 8 disparities as packed pairs (104 registers at rho = 6), so
+//    every staged cost feeds 2 rho + 1 FFMA2s.  Ages shift by one per input
+//    row inside the last tap's FFMA2s (destination = next-younger register),
+//    so the loop needs no unrolling over ages and no register moves.
+//  * Warp roles (mbarrier hand-off, no CTA barrier inside a segment): G
+//    consumer warps (FFMA2, fma.rn.f32x2 with a scalar weight operand),
+//    3 weight-producer warps (exp2 on the MUFU pipe, once per (pixel, tap) per
+//    CTA, per-pixel weight sums), 1 stager warp (cost rows by cp.async.bulk,
+//    the TMA engine, 4-stage ring).
+//  * Persistent CTAs: one CTA per SM walks an equal share of the linearised
+//    (frame, slab, strip, row) space in segments of <= 720 rows, so the grid
+//    has no wave-quantisation tail and a strip pays its 2 rho warm-up rows once
+//    per segment.
+//  * Tiles whose footprint holds no partially-NaN pixel (nan_map) take the
+//    "clean" path: NaN-free costs (all-NaN or outside pixels get weight 0 and
+//    cost 0) and one denominator per pixel.  Other segments take the exact
+//    general path: pairs (C0, V) = (cost or 0, validity) so the same FFMA2
+//    accumulates numerator and per-disparity denominator, two passes per slab.
+#include <cuda_fp16.h>
+
 #include <cmath>
 
 #include "common.cuh"
@@ -29,43 +43,35 @@
 
 namespace rsr {
 
-constexpr int SL_KT = 8;        // disparities per consumer thread
-constexpr int SL_NPROD = 3;     // weight-producer warps (+1 stager warp)
-constexpr int SL_NSC = 4;       // cost stages
-constexpr int SL_NSW = 3;       // weight stages
-constexpr int SL_ROWS = 180;    // output rows per CTA chunk
+constexpr int SG_NPROD = 4;     // weight-producer warps (warp 0 also stages costs)
+constexpr int SG_NSC = 4;       // cost stages
+constexpr int SG_NSW = 3;       // weight stages
+constexpr int SG_SEGMAX = 720;  // max output rows per segment (guide tile height)
 
 struct SlideGeom {
-  int n_kg, KS, DPAD, CX, WX, WSTAGE, GR, GC, nslab, R;
-  size_t off_cost, off_w, off_dsum, off_guide, off_bar, bytes;
+  int G, KS, nslab, CX, XS, WST, GR;
+  size_t off_cost, off_w, off_dpart, off_guide, off_bar, bytes;
 };
 
-// cost stage: [CX columns][KS + 4] raw fp32 costs (NaN = invalid)
-// weight stage: [32 x][NT taps][16 ages] (x stride padded to 4*odd floats)
-// + dsum partials [SL_NPROD][32]
-__host__ __device__ inline SlideGeom slide_geom(int D, int rho, int H) {
+// KS = disparities per slab (multiple of 8, <= 64), G = consumer lanes per column
+__host__ __device__ inline SlideGeom slide_geom(int D, int rho) {
   SlideGeom g;
   const int NT = 2 * rho + 1;
-  const int ks = D < 64 ? D : 64;
-  g.n_kg = (ks + SL_KT - 1) / SL_KT;
-  g.KS = g.n_kg * SL_KT;
-  g.DPAD = g.KS + 4;
+  g.nslab = (D + 63) / 64;
+  const int per = (D + g.nslab - 1) / g.nslab;
+  g.KS = (per + 7) & ~7;
+  g.G = g.KS / 8;
   g.CX = 32 + 2 * rho;
-  int wx = NT * 16;
-  if (((wx / 4) & 1) == 0) wx += 4;
-  g.WX = wx;
-  g.WSTAGE = 32 * g.WX + SL_NPROD * 32;
-  g.R = SL_ROWS < H ? SL_ROWS : H;
-  g.GR = g.R + 4 * rho;   // output rows y in [Y0 - 2 rho, Y1 + 2 rho)
-  g.GC = 32 + 2 * rho;
-  g.nslab = (D + g.KS - 1) / g.KS;
+  g.XS = 16 * NT + 4;                 // == 20 (mod 32): 4 / 8 columns hit distinct banks
+  g.WST = 32 * g.XS + 32;             // weights [x][tap][age16] + completing rows' weight sums
+  g.GR = SG_SEGMAX + 4 * rho;
   size_t o = 0;
-  g.off_cost = o; o += sizeof(float) * (size_t)SL_NSC * g.CX * g.DPAD;
-  g.off_w = o;    o += sizeof(float) * (size_t)SL_NSW * g.WSTAGE;
-  g.off_dsum = o; o += sizeof(float) * (size_t)SL_NPROD * NT * 32;
-  g.off_guide = o; o += sizeof(float) * (size_t)g.GR * g.GC;
+  g.off_cost = o;  o += sizeof(float) * (size_t)SG_NSC * g.CX * g.KS;
+  g.off_w = o;     o += sizeof(float) * (size_t)SG_NSW * g.WST;
+  g.off_dpart = o; o += sizeof(float) * (size_t)NT * 32;
+  g.off_guide = o; o += sizeof(__half) * (size_t)g.GR * g.CX;
   o = (o + 15) & ~size_t(15);
-  g.off_bar = o;  o += 8 * (2 * SL_NSC + 2 * SL_NSW) + 16;
+  g.off_bar = o;   o += 8 * (2 * SG_NSC + 2 * SG_NSW);
   g.bytes = o;
   return g;
 }
@@ -74,239 +80,300 @@ RSR_DEVINL void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Per-CTA context shared by the three warp roles.
-struct SlideCtx {
-  SlideGeom g;
-  float* cost_s;
-  float* w_s;
-  float* dsum_s;
-  float* guide_s;
-  uint64_t *full_c, *empty_c, *full_w, *empty_w;
-  const float* vol;
-  float* out;
-  int H, W, D, x0, Y0, Y1, k0, ks_eff, NR, lane;
+// d = w * c + a on a packed pair (FFMA2 with scalar-broadcast weight operand)
+RSR_DEVINL float2 fma2s(float w, float2 c, float2 a) {
+  unsigned long long av, cv, wb, dv;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(av) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(cv) : "f"(c.x), "f"(c.y));
+  asm("mov.b64 %0, {%1,%1};" : "=l"(wb) : "f"(w));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(dv) : "l"(wb), "l"(cv), "l"(av));
+  float2 d;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(dv));
+  return d;
+}
+
+// One output segment: rows [ya, yb) of strip x0 of frame b, disparity slab k0.
+struct Seg {
+  int b, k0, ks_eff, x0, ya, yb;
   size_t pix0;
-  float kd, kr;
-  bool clean;
 };
 
-// ---- stager (1 warp): raw cost rows into stage it % NSC.  One bulk copy per
-// in-image pixel column (TMA engine); skipped columns (outside the image, or
-// all-NaN on a clean chunk) are filled with 0 (clean) or NaN (general path).
+struct SlideArgs {
+  int B, H, W, D;
+  int R;                 // output rows per CTA (<= SG_SEGMAX)
+  float kd, kr;
+  const float* vol;
+  const uint8_t* guide;
+  const uint8_t* nan_map;
+  float* out;
+};
+
+// The CTA's segment: blockIdx.x = strip, blockIdx.y = row chunk of R rows,
+// blockIdx.z = frame * nslab + slab.  The hardware block scheduler balances
+// clean and (twice as expensive) general-path segments across the SMs.
+RSR_DEVINL Seg cta_segment(const SlideArgs& A, const SlideGeom& g) {
+  Seg s;
+  s.x0 = blockIdx.x * 32;
+  s.ya = blockIdx.y * A.R;
+  s.yb = min(A.H, s.ya + A.R);
+  s.b = blockIdx.z / g.nslab;
+  s.k0 = (blockIdx.z % g.nslab) * g.KS;
+  s.ks_eff = min(g.KS, A.D - s.k0);
+  s.pix0 = (size_t)s.b * A.H * A.W;
+  return s;
+}
+
+// ---- stager (lanes of producer warp 0): raw cost row i of the segment into
+// the cost ring.  One bulk async copy (TMA engine) per in-image pixel column,
+// or one for the whole row segment when it is contiguous; skipped columns
+// (outside the image, or all-NaN on a clean segment) are filled with 0 (clean)
+// or NaN (general path).
 template <int RHO>
-__device__ __noinline__ void slide_stager(const SlideCtx c, int npass) {
-  const SlideGeom& g = c.g;
-  const int lane = c.lane;
-  const bool bulk = (c.D & 3) == 0;
-  uint32_t it_c = 0;
-  for (int pass = 0; pass < npass; pass++) {
-    for (int i = 0; i < c.NR; i++, it_c++) {
-      const int st = it_c % SL_NSC;
-      if (it_c >= SL_NSC) mbar_wait_parity(&c.empty_c[st], ((it_c / SL_NSC) & 1) ^ 1);
-      const int yy = c.Y0 - RHO + i;
-      float* dst = c.cost_s + (size_t)st * g.CX * g.DPAD;
-      const bool row_in = yy >= 0 && yy < c.H;
-      const float* gtile = c.guide_s + (i + RHO) * g.GC;   // same row / columns as the stage
-      const float fillv = c.clean ? 0.f : qnan();
-      // each lane owns columns lane and lane + 32 (CX <= 46)
-      bool copy_col[2];
+__device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g, const Seg& s, bool clean,
+                                          int i, const __half* gt, float* cost_s, uint64_t* full_c, uint64_t* empty_c,
+                                          uint32_t& it_c, int lane) {
+  const bool bulk = (A.D & 3) == 0;
+  const float fillv = clean ? 0.f : qnan();
+  const int st = it_c % SG_NSC;
+  if (it_c >= SG_NSC) mbar_wait_parity(&empty_c[st], ((it_c / SG_NSC) & 1) ^ 1);
+  it_c++;
+  const int yy = s.ya - RHO + i;
+  float* dst = cost_s + (size_t)st * g.CX * g.KS;
+  const bool row_in = yy >= 0 && yy < A.H;
+  const size_t rowpix = s.pix0 + (size_t)yy * A.W;
+  bool cp[2];
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int col = lane + 32 * h;
-        const int xx = c.x0 - RHO + col;
-        const bool in = col < g.CX && row_in && xx >= 0 && xx < c.W;
-        copy_col[h] = in && bulk && !(c.clean && gtile[col] != gtile[col]);
-        if (col < g.CX && !copy_col[h]) {
-          float* d = dst + col * g.DPAD;
-          if (in && !bulk) {
-            const float* sp = c.vol + (c.pix0 + (size_t)yy * c.W + xx) * c.D + c.k0;
-            for (int k = 0; k < g.KS; k++) d[k] = (c.k0 + k < c.D) ? sp[k] : qnan();
+  for (int h = 0; h < 2; h++) {
+    const int col = lane + 32 * h;
+    const int xx = s.x0 - RHO + col;
+    // the guide tile marks outside and all-NaN pixels (+inf): fill them instead of copying
+    // (all-NaN -> 0 on a clean segment, where such taps carry weight 0; NaN otherwise)
+    const bool skip = !(col < g.CX && row_in) || __hisinf(gt[(i + RHO) * g.CX + col]) != 0;
+    cp[h] = !skip && bulk;
+    if (col < g.CX) {
+      float* d = dst + col * g.KS;
+      if (!skip && !bulk) {
+        const float* sp = A.vol + (rowpix + xx) * A.D + s.k0;
+        for (int k = 0; k < g.KS; k++) d[k] = k < s.ks_eff ? sp[k] : fillv;
+      } else if (skip) {
+        for (int k = 0; k < g.KS; k += 4) *reinterpret_cast<float4*>(d + k) = make_float4(fillv, fillv, fillv, fillv);
+      } else if (s.ks_eff < g.KS) {
+        for (int k = s.ks_eff; k < g.KS; k++) d[k] = fillv;   // slab tail (the copy fills the head)
+      }
+    }
+  }
+  const uint32_t ncols = __popc(__ballot_sync(0xffffffffu, cp[0])) + __popc(__ballot_sync(0xffffffffu, cp[1]));
+  __syncwarp();
+  const float* src = A.vol + (rowpix + (s.x0 - RHO)) * A.D + s.k0;
+  if (ncols == (uint32_t)g.CX && g.KS == A.D) {
+    // whole row segment in the image and one contiguous run: a single bulk copy
+    const uint32_t bytes = (uint32_t)g.CX * g.KS * 4u;
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&full_c[st], bytes);
+      bulk_g2s(dst, src, bytes, &full_c[st]);
+    }
+  } else {
+    const uint32_t bytes_col = (uint32_t)s.ks_eff * 4u;
+    if (lane == 0) mbar_arrive_expect_tx(&full_c[st], bytes_col * ncols);
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int col = lane + 32 * h;
+      if (cp[h]) bulk_g2s(dst + col * g.KS, src + (size_t)col * A.D, bytes_col, &full_c[st]);
+    }
+  }
+}
+
+// ---- weight producers (SG_NPROD warps): weights of input row r for the
+// 2 rho + 1 output rows (ages) whose windows contain it,
+//   w[x][j][age] = exp2(kd (dx^2 + dy^2) + kr (g(q) - g(p))^2),
+// and the per-pixel weight sums.  A lane owns (column x, age a) over 8 columns
+// x 4 ages (conflict-free 4-byte stores into the [x][tap][age] layout) and
+// walks the taps j in order, so the running sum of an output row's weights is
+// accumulated in exactly the (input row, tap) order in which the general path's
+// FFMA2 accumulates its per-disparity denominators: both paths give bitwise
+// identical results wherever both apply, whatever the segmentation (batch-size
+// independence).  Warp 0 also stages the cost rows.
+template <int RHO>
+__device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideGeom& g, const Seg& s,
+                                                bool clean, int npass, const __half* gt, float* w_s,
+                                                float* dsum, float* cost_s, uint64_t* full_w,
+                                                uint64_t* empty_w, uint64_t* full_c, uint64_t* empty_c,
+                                                uint32_t& it_w, uint32_t& it_c, int p, int lane) {
+  constexpr int NT = 2 * RHO + 1;
+  constexpr int NAB = (NT + 3) / 4;          // age blocks of 4
+  const int NR = (s.yb - s.ya) + 2 * RHO;
+  const int xs = lane >> 2, as = lane & 3;
+  for (int pass = 0; pass < npass; pass++) {
+    for (int e = p * 32 + lane; e < NT * 32; e += SG_NPROD * 32) dsum[e] = 0.f;
+    asm volatile("bar.sync 1, %0;" ::"r"(SG_NPROD * 32) : "memory");
+    for (int i = 0; i < NR; i++, it_w++) {
+      if (p == 0) stage_row<RHO>(A, g, s, clean, i, gt, cost_s, full_c, empty_c, it_c, lane);
+      const int st = it_w % SG_NSW;
+      if (it_w >= SG_NSW) mbar_wait_parity(&empty_w[st], ((it_w / SG_NSW) & 1) ^ 1);
+      float* wst = w_s + (size_t)st * g.WST;
+      const __half* trow = gt + (i + RHO) * g.CX;   // tap row r
+      // this warp's items (x-block, age-block) = p + 4 n, n < NAB; all shared-memory
+      // loads first, then the math, then the stores: the tile, the running sums and
+      // the weight stage may alias as far as the compiler knows, so interleaving them
+      // would serialise every tap's LDS -> MUFU -> STS chain
+      static_assert(SG_NPROD == 4, "items are dealt to 4 producer warps");
+      float wv[NAB][NT], gp[NAB], den[NAB];
+#pragma unroll
+      for (int n = 0; n < NAB; n++) {
+        const int item = p + 4 * n;
+        const int x = (item / NAB) * 8 + xs, a = min((item % NAB) * 4 + as, NT - 1);
+        // centre of age a: output row r - RHO + a = guide tile row i + a, column x + RHO.
+        // Skipped pixels (outside / all-NaN) are +inf in the tile and -inf as a centre,
+        // so dg = +-inf and every weight touching them is exp2(-inf) = 0 exactly
+        // (kr < 0 also for gamma_r = inf, where kr = -1e-30).
+        const float cg = __half2float(gt[(i + a) * g.CX + x + RHO]);
+        gp[n] = isinf(cg) ? -cg : cg;
+        den[n] = dsum[((i + a) % NT) * 32 + x];
+#pragma unroll
+        for (int j = 0; j < NT; j++) wv[n][j] = __half2float(trow[x + j]);
+      }
+#pragma unroll
+      for (int n = 0; n < NAB; n++) {
+        const int a = min(((p + 4 * n) % NAB) * 4 + as, NT - 1);
+        const float cy = (float)((RHO - a) * (RHO - a)) * A.kd;
+#pragma unroll
+        for (int j = 0; j < NT; j++) {
+          const float dg = wv[n][j] - gp[n];
+          wv[n][j] = ex2_ftz(fmaf(dg * A.kr, dg, (float)((j - RHO) * (j - RHO)) * A.kd + cy));
+        }
+      }
+#pragma unroll
+      for (int n = 0; n < NAB; n++) {
+        const int item = p + 4 * n;
+        const int x = (item / NAB) * 8 + xs, a = (item % NAB) * 4 + as;
+        if (a < NT) {
+          float* wd = wst + x * g.XS + a;
+          float d = den[n];
+#pragma unroll
+          for (int j = 0; j < NT; j++) {
+            wd[j * 16] = wv[n][j];
+            d += wv[n][j];
+          }
+          if (a == 0) {   // the output row completing at input row i
+            wst[32 * g.XS + x] = d;
+            dsum[((i + a) % NT) * 32 + x] = 0.f;
           } else {
-            for (int k = 0; k < g.KS; k += 4) *reinterpret_cast<float4*>(d + k) = make_float4(fillv, fillv, fillv, fillv);
+            dsum[((i + a) % NT) * 32 + x] = d;
           }
         }
       }
-      const uint32_t ncols = __popc(__ballot_sync(0xffffffffu, copy_col[0])) +
-                             __popc(__ballot_sync(0xffffffffu, copy_col[1]));
-      __syncwarp();
-      const uint32_t bytes_col = (uint32_t)c.ks_eff * 4u;
-      if (lane == 0) mbar_arrive_expect_tx(&c.full_c[st], bytes_col * ncols);
-      __syncwarp();
-      const float* src = c.vol + ((c.pix0 + (size_t)yy * c.W + (c.x0 - RHO)) * c.D + c.k0);
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int col = lane + 32 * h;
-        if (copy_col[h]) bulk_g2s(dst + col * g.DPAD, src + (size_t)col * c.D, bytes_col, &c.full_c[st]);
-      }
+      asm volatile("bar.sync 1, %0;" ::"r"(SG_NPROD * 32) : "memory");   // row sums handed to the next age
+      mbar_arrive(&full_w[st]);
     }
   }
 }
 
-// ---- weight producers (SL_NPROD warps): weights of input row i in age order,
-// w[x][tap][age] = exp2(kd (dx^2 + dy^2) + kr (g(q) - g(p))^2), 0 for a skipped
-// tap (NaN guide); per-pixel weight sums per output row.
-template <int RHO>
-__device__ __noinline__ void slide_weights(const SlideCtx c, int p, int npass) {
-  constexpr int NT = 2 * RHO + 1;
-  const SlideGeom& g = c.g;
-  const int x = c.lane;
-  float* dpart = c.dsum_s + (size_t)p * NT * 32;   // [row slot][x] ring, private to warp p
-  uint32_t it_w = 0;
-  for (int pass = 0; pass < npass; pass++) {
-    for (int a = 0; a < NT; a++) dpart[a * 32 + x] = 0.f;
-    for (int i = 0; i < c.NR; i++, it_w++) {
-      const int st = it_w % SL_NSW;
-      if (it_w >= SL_NSW) mbar_wait_parity(&c.empty_w[st], ((it_w / SL_NSW) & 1) ^ 1);
-      float* wst = c.w_s + (size_t)st * g.WSTAGE;
-      const float* grow = c.guide_s + (i + RHO) * g.GC + x;   // input row r, column x - RHO
-      // age a (0 = oldest) holds output row y = r - RHO + a, i.e. dy = r - y = RHO - a;
-      // its guide value g(x, y) sits in guide tile row y - (Y0 - 2 RHO) = i + a.
-      // Skipped pixels (NaN in the guide tile) are re-encoded so that their weight
-      // underflows to exactly 0 without a branch: -1e18 as a centre, +1e18 as a tap
-      // (|dg| >= 1e18 - 255, kr dg^2 <= -1e6 even for gamma_r = inf where kr = -1e-30).
-      float gp[NT];
-#pragma unroll
-      for (int a = 0; a < NT; a++) {
-        const float v = c.guide_s[(i + a) * g.GC + x + RHO];
-        gp[a] = (v != v) ? -1e18f : v;
-      }
-      float cy[NT];
-#pragma unroll
-      for (int a = 0; a < NT; a++) cy[a] = (float)((RHO - a) * (RHO - a)) * c.kd;
-      float dpa[NT];
-#pragma unroll
-      for (int a = 0; a < NT; a++) dpa[a] = 0.f;
-      for (int j = p; j < NT; j += SL_NPROD) {
-        const float gv = grow[j];
-        const float gq = (gv != gv) ? 1e18f : gv;
-        const float cx = (float)((j - RHO) * (j - RHO)) * c.kd;
-        float wv[16];
-#pragma unroll
-        for (int a = 0; a < NT; a++) {
-          const float dg = gq - gp[a];
-          const float arg = fmaf(dg * c.kr, dg, cx + cy[a]);
-          wv[a] = ex2_approx(arg);
-          dpa[a] += wv[a];
-        }
-#pragma unroll
-        for (int a = NT; a < 16; a++) wv[a] = 0.f;
-        float4* d4 = reinterpret_cast<float4*>(wst + x * g.WX + j * 16);
-#pragma unroll
-        for (int q = 0; q < 4; q++) d4[q] = make_float4(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
-      }
-      // running per-pixel weight sums per output row; row y = Y0 - 2 RHO + i + a
-      // lives in ring slot (i + a) % NT (the consumers' register slot as well)
-#pragma unroll
-      for (int a = 0; a < NT; a++) dpart[((i + a) % NT) * 32 + x] += dpa[a];
-      // row completing at input row i: age 0, slot i % NT
-      const int cs = i % NT;
-      wst[32 * g.WX + p * 32 + x] = dpart[cs * 32 + x];
-      dpart[cs * 32 + x] = 0.f;
-      mbar_arrive(&c.full_w[st]);
-    }
-  }
-}
-
-// ---- consumers (one warp per 8 disparities): sliding accumulation ----
+// ---- consumers (G warps): sliding accumulation, FFMA2 -----------------------
 template <int RHO, bool CLEAN>
-__device__ __forceinline__ void slide_consume(const SlideCtx& c, int kg) {
+__device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, const Seg& s,
+                                        const float* cost_s, const float* w_s, uint64_t* full_c,
+                                        uint64_t* empty_c, uint64_t* full_w, uint64_t* empty_w,
+                                        uint32_t& it, int xl, int l, int lane) {
   constexpr int NT = 2 * RHO + 1;
   constexpr int NPASS = CLEAN ? 1 : 2;
-  const SlideGeom& g = c.g;
-  const int lane = c.lane;
-  const int x = c.x0 + lane;
-  uint32_t it = 0;
+  const int NR = (s.yb - s.ya) + 2 * RHO;
+  const int x = s.x0 + xl;
+  const bool vec_out = (A.D & 3) == 0;
   for (int pass = 0; pass < NPASS; pass++) {
-    float2 acc[NT][SL_KT / 2];
+    float2 acc[NT][4];
 #pragma unroll
     for (int a = 0; a < NT; a++)
 #pragma unroll
-      for (int q = 0; q < SL_KT / 2; q++) acc[a][q] = make_float2(0.f, 0.f);
-
-    for (int base = 0; base < c.NR; base += NT) {
+      for (int q = 0; q < 4; q++) acc[a][q] = make_float2(0.f, 0.f);
+    // this lane's disparities: clean {4l..4l+3} U {4G+4l..}, general pass h: {4Gh + 4l..}
+    const int koff = CLEAN ? 4 * l : 4 * g.G * pass + 4 * l;
+    for (int i = 0; i < NR; i++, it++) {
+      const int stc = it % SG_NSC, stw = it % SG_NSW;
+      mbar_wait_parity(&full_c[stc], (it / SG_NSC) & 1);
+      mbar_wait_parity(&full_w[stw], (it / SG_NSW) & 1);
+      const float* crow = cost_s + (size_t)stc * g.CX * g.KS + xl * g.KS + koff;
+      const float* wrow = w_s + (size_t)stw * g.WST + xl * g.XS;
+      float2 fin[4];
 #pragma unroll
-      for (int u = 0; u < NT; u++) {
-        const int i = base + u;
-        if (i < c.NR) {
-          const int stc = it % SL_NSC, stw = it % SL_NSW;
-          mbar_wait_parity(&c.full_c[stc], (it / SL_NSC) & 1);
-          mbar_wait_parity(&c.full_w[stw], (it / SL_NSW) & 1);
-          const float* crow = c.cost_s + (size_t)stc * g.CX * g.DPAD + lane * g.DPAD + kg * SL_KT;
-          const float* wrow = c.w_s + (size_t)stw * g.WSTAGE + lane * g.WX;
+      for (int j = 0; j < NT; j++) {
+        float2 cp[4];
+        if (CLEAN) {
+          const float4 ca = *reinterpret_cast<const float4*>(crow + j * g.KS);
+          const float4 cb = *reinterpret_cast<const float4*>(crow + j * g.KS + 4 * g.G);
+          cp[0] = make_float2(ca.x, ca.y); cp[1] = make_float2(ca.z, ca.w);
+          cp[2] = make_float2(cb.x, cb.y); cp[3] = make_float2(cb.z, cb.w);
+        } else {
+          const float4 t = *reinterpret_cast<const float4*>(crow + j * g.KS);
+          const float tv[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
-          for (int j = 0; j < NT; j++) {
-            float2 cp[4];
-            if (CLEAN) {
-              const float4* c4 = reinterpret_cast<const float4*>(crow + j * g.DPAD);
-              const float4 ca = c4[0], cb = c4[1];
-              cp[0] = make_float2(ca.x, ca.y); cp[1] = make_float2(ca.z, ca.w);
-              cp[2] = make_float2(cb.x, cb.y); cp[3] = make_float2(cb.z, cb.w);
+          for (int q = 0; q < 4; q++) {
+            const bool ok = !(tv[q] != tv[q]);
+            cp[q] = make_float2(ok ? tv[q] : 0.f, ok ? 1.f : 0.f);
+          }
+        }
+        float wv[16];
+        const float4* w4 = reinterpret_cast<const float4*>(wrow + j * 16);
+#pragma unroll
+        for (int q = 0; q < (NT + 3) / 4; q++) {
+          const float4 t = w4[q];
+          wv[4 * q] = t.x; wv[4 * q + 1] = t.y; wv[4 * q + 2] = t.z; wv[4 * q + 3] = t.w;
+        }
+        if (j < NT - 1) {
+#pragma unroll
+          for (int a = 0; a < NT; a++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) acc[a][q] = fma2s(wv[a], cp[q], acc[a][q]);
+        } else {
+          // last tap of the row: age 0 completes, every other age moves one slot down
+#pragma unroll
+          for (int q = 0; q < 4; q++) fin[q] = fma2s(wv[0], cp[q], acc[0][q]);
+#pragma unroll
+          for (int a = 1; a < NT; a++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) acc[a - 1][q] = fma2s(wv[a], cp[q], acc[a][q]);
+#pragma unroll
+          for (int q = 0; q < 4; q++) acc[NT - 1][q] = make_float2(0.f, 0.f);
+        }
+      }
+      const float den = CLEAN ? wrow[(32 - xl) * g.XS + xl] : 0.f;
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&empty_c[stc]);
+        mbar_arrive(&empty_w[stw]);
+      }
+      const int y = s.ya - 2 * RHO + i;   // completing output row
+      if (y >= s.ya && x < A.W) {
+        const size_t pix = s.pix0 + (size_t)y * A.W + x;
+        float* o = A.out + pix * A.D + s.k0 + koff;
+        if (CLEAN) {
+          // den == 0 exactly when the centre is skipped (all-NaN): 0 * inf = NaN
+          const float inv = __frcp_rn(den);
+          const float r[8] = {fin[0].x * inv, fin[0].y * inv, fin[1].x * inv, fin[1].y * inv,
+                              fin[2].x * inv, fin[2].y * inv, fin[3].x * inv, fin[3].y * inv};
+#pragma unroll
+          for (int hh = 0; hh < 2; hh++) {
+            const int kb = s.k0 + koff + 4 * g.G * hh;
+            float* oh = o + 4 * g.G * hh;
+            if (vec_out && kb + 3 < A.D) {
+              *reinterpret_cast<float4*>(oh) = make_float4(r[4 * hh], r[4 * hh + 1], r[4 * hh + 2], r[4 * hh + 3]);
             } else {
-              // (C0, V): cost or 0, validity, for k = k0 + 8 kg + 4 pass + q
-              const float4 t = *reinterpret_cast<const float4*>(crow + j * g.DPAD + 4 * pass);
-              const float tv[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
-              for (int q = 0; q < 4; q++) {
-                const bool ok = !(tv[q] != tv[q]);
-                cp[q] = make_float2(ok ? tv[q] : 0.f, ok ? 1.f : 0.f);
-              }
-            }
-            const float4* w4 = reinterpret_cast<const float4*>(wrow + j * 16);
-            float wv[16];
-#pragma unroll
-            for (int q = 0; q < (NT + 3) / 4; q++) {
-              const float4 t = w4[q];
-              wv[4 * q] = t.x; wv[4 * q + 1] = t.y; wv[4 * q + 2] = t.z; wv[4 * q + 3] = t.w;
-            }
-#pragma unroll
-            for (int a = 0; a < NT; a++) {
-              // age a lives in register slot (u + a) % NT
-#pragma unroll
-              for (int q = 0; q < 4; q++) ffma2_bcast(acc[(u + a) % NT][q], wv[a], cp[q]);
+              for (int q = 0; q < 4; q++)
+                if (kb + q < A.D) oh[q] = r[4 * hh + q];
             }
           }
-          // completing output row: age 0, slot u, image row y = Y0 - 2 RHO + i
-          const int y = c.Y0 - 2 * RHO + i;
-          float den = 0.f;
-          if (CLEAN) {
-            const float* dsrc = c.w_s + (size_t)stw * g.WSTAGE + 32 * g.WX;
+        } else {
+          const float* cv = A.vol + pix * A.D + s.k0 + koff;
+          const float fv[8] = {fin[0].x, fin[0].y, fin[1].x, fin[1].y, fin[2].x, fin[2].y, fin[3].x, fin[3].y};
 #pragma unroll
-            for (int pp = 0; pp < SL_NPROD; pp++) den += dsrc[pp * 32 + lane];
-          }
-          __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&c.empty_c[stc]);
-            mbar_arrive(&c.empty_w[stw]);
-          }
-          it++;
-          if (y >= c.Y0 && y < c.Y1 && x < c.W) {
-            float* o = c.out + (c.pix0 + (size_t)y * c.W + x) * c.D;
-            if (CLEAN) {
-              // den == 0 exactly when the centre pixel is skipped (all-NaN): 0 * inf = NaN
-              const int kb = c.k0 + kg * SL_KT;
-              const float inv = 1.f / den;
-#pragma unroll
-              for (int q2 = 0; q2 < 2; q2++) {
-                if (kb + 4 * q2 < c.D) {
-                  const float2 a0 = acc[u][2 * q2], a1 = acc[u][2 * q2 + 1];
-                  *reinterpret_cast<float4*>(o + kb + 4 * q2) =
-                      make_float4(a0.x * inv, a0.y * inv, a1.x * inv, a1.y * inv);
-                }
-              }
-            } else {
-              const int kb = c.k0 + kg * SL_KT + 4 * pass;
-#pragma unroll
-              for (int q = 0; q < 4; q++) {
-                const int k = kb + q;
-                if (k < c.D) {
-                  const float cv = c.vol[(c.pix0 + (size_t)y * c.W + x) * c.D + k];
-                  o[k] = (cv != cv) ? qnan() : acc[u][q].x / acc[u][q].y;
-                }
-              }
+          for (int q = 0; q < 4; q++) {
+            const int k = s.k0 + koff + q;
+            if (k < s.k0 + s.ks_eff) {
+              const float c = cv[q];
+              o[q] = (c != c) ? qnan() : fv[2 * q] * __frcp_rn(fv[2 * q + 1]);
             }
           }
-#pragma unroll
-          for (int q = 0; q < 4; q++) acc[u][q] = make_float2(0.f, 0.f);
         }
       }
     }
@@ -314,120 +381,110 @@ __device__ __forceinline__ void slide_consume(const SlideCtx& c, int kg) {
 }
 
 template <int RHO>
-__global__ void __launch_bounds__(384, 1)
-    k_aggregate_slide(int H, int W, int D, float kd, float kr, const float* __restrict__ vol,
-                      const uint8_t* __restrict__ guide, const uint8_t* __restrict__ nan_map,
-                      float* __restrict__ out) {
-  extern __shared__ __align__(16) unsigned char sl_smem[];
-  SlideCtx c;
-  c.g = slide_geom(D, RHO, H);
-  const SlideGeom& g = c.g;
-  c.cost_s = reinterpret_cast<float*>(sl_smem + g.off_cost);
-  c.w_s = reinterpret_cast<float*>(sl_smem + g.off_w);
-  c.dsum_s = reinterpret_cast<float*>(sl_smem + g.off_dsum);
-  c.guide_s = reinterpret_cast<float*>(sl_smem + g.off_guide);
-  c.full_c = reinterpret_cast<uint64_t*>(sl_smem + g.off_bar);
-  c.empty_c = c.full_c + SL_NSC;
-  c.full_w = c.empty_c + SL_NSC;
-  c.empty_w = c.full_w + SL_NSW;
-  c.vol = vol;
-  c.out = out;
-  c.H = H; c.W = W; c.D = D; c.kd = kd; c.kr = kr;
+__global__ void __launch_bounds__(384, 1) k_aggregate_slide(const SlideArgs A) {
+  extern __shared__ __align__(128) unsigned char sl_smem[];
+  const SlideGeom g = slide_geom(A.D, RHO);
+  float* cost_s = reinterpret_cast<float*>(sl_smem + g.off_cost);
+  float* w_s = reinterpret_cast<float*>(sl_smem + g.off_w);
+  float* dpart = reinterpret_cast<float*>(sl_smem + g.off_dpart);
+  __half* gt = reinterpret_cast<__half*>(sl_smem + g.off_guide);
+  uint64_t* full_c = reinterpret_cast<uint64_t*>(sl_smem + g.off_bar);
+  uint64_t* empty_c = full_c + SG_NSC;
+  uint64_t* full_w = empty_c + SG_NSC;
+  uint64_t* empty_w = full_w + SG_NSW;
 
-  const int tid = threadIdx.x, warp = tid >> 5;
-  c.lane = tid & 31;
-  // warpgroups: consumers in warps [0, n_cons) (n_kg working, padded to a multiple
-  // of 4), then one producer warpgroup: SL_NPROD weight warps, the stager, padding.
-  const int n_cons = (g.n_kg + 3) & ~3;
-  c.x0 = blockIdx.x * 32;
-  c.Y0 = blockIdx.y * g.R;
-  c.Y1 = min(H, c.Y0 + g.R);
-  const int b = blockIdx.z / g.nslab, slab = blockIdx.z % g.nslab;
-  c.k0 = slab * g.KS;
-  c.ks_eff = min(g.KS, D - c.k0);
-  c.pix0 = (size_t)b * H * W;
-  c.NR = (c.Y1 - c.Y0) + 2 * RHO;           // input rows r = Y0 - RHO + i, i in [0, NR)
-
-  // ---- classify the chunk ----
-  // nan_map byte: bit 0 = some disparity NaN, bit 1 = some disparity finite.
-  // Pixels with every disparity NaN (m == 1) and pixels outside the image are
-  // exact to handle on the clean path: their taps get weight 0 (skipped) and
-  // their outputs come out NaN (0 / 0).  Only a pixel with SOME NaN (m == 3)
-  // needs per-disparity denominators, i.e. the (C0, V) path.
-  bool clean = (nan_map != nullptr) && ((D & 3) == 0);
-  if (clean) {
-    int partial = 0;
-    const int fw = 32 + 2 * RHO;
-    for (int i = tid; i < c.NR * fw; i += blockDim.x) {
-      const int yy = c.Y0 - RHO + i / fw, xx = c.x0 - RHO + i % fw;
-      if (yy >= 0 && yy < H && xx >= 0 && xx < W) partial |= (nan_map[c.pix0 + (size_t)yy * W + xx] == 3);
-    }
-    clean = !__syncthreads_or(partial);
-  }
-  c.clean = clean;
-  // guide rows [Y0 - 2 RHO, Y0 - 2 RHO + GR), columns [x0 - RHO, x0 + 32 + RHO);
-  // NaN marks a pixel whose taps are skipped (outside the image, or all-NaN costs)
-  for (int i = tid; i < g.GR * g.GC; i += blockDim.x) {
-    const int yy = c.Y0 - 2 * RHO + i / g.GC, xx = c.x0 - RHO + i % g.GC;
-    float gv = qnan();
-    if (yy >= 0 && yy < H && xx >= 0 && xx < W) {
-      const size_t pi = c.pix0 + (size_t)yy * W + xx;
-      if (nan_map == nullptr || nan_map[pi] != 1) gv = (float)guide[pi];
-    }
-    c.guide_s[i] = gv;
-  }
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_cons = g.G;   // consumer warps
   if (tid == 0) {
-    for (int s = 0; s < SL_NSC; s++) {
-      mbar_init(&c.full_c[s], 1);
-      mbar_init(&c.empty_c[s], g.n_kg);
+    for (int q = 0; q < SG_NSC; q++) {
+      mbar_init(&full_c[q], 1);
+      mbar_init(&empty_c[q], n_cons);
     }
-    for (int s = 0; s < SL_NSW; s++) {
-      mbar_init(&c.full_w[s], 32 * SL_NPROD);
-      mbar_init(&c.empty_w[s], g.n_kg);
+    for (int q = 0; q < SG_NSW; q++) {
+      mbar_init(&full_w[q], 32 * SG_NPROD);
+      mbar_init(&empty_w[q], n_cons);
     }
     fence_mbar_init();
   }
-  __syncthreads();
-
-  if (warp >= n_cons) {
-    // ======================= producer warpgroup =======================
-    // register budget per lane-slot: the CTA holds 3 x 168 = 504 (launch bound 384);
-    // producers give back to 88 so both consumer warpgroups can grow to 208.
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
-    const int p = warp - n_cons;
-    if (p < SL_NPROD)
-      slide_weights<RHO>(c, p, clean ? 1 : 2);
-    else if (p == SL_NPROD)
-      slide_stager<RHO>(c, clean ? 1 : 2);
-  } else {
-    // ======================= consumer warpgroups =======================
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
-    if (warp < g.n_kg) {
+  uint32_t it = 0, it_c = 0;   // per-role running row counters (mbarrier phases continue across segments)
+  {
+    const Seg s = cta_segment(A, g);
+    // ---- classify the segment and load its guide tile ----
+    // nan_map byte: bit 0 = some disparity NaN, bit 1 = some disparity finite.  Only a
+    // partially-NaN pixel (3) needs per-disparity denominators (the general path).
+    int partial = (A.nan_map == nullptr) ? 1 : 0;
+    const int rows = (s.yb - s.ya) + 4 * RHO;
+    for (int e = tid; e < rows * g.CX; e += blockDim.x) {
+      const int yy = s.ya - 2 * RHO + e / g.CX, xx = s.x0 - RHO + e % g.CX;
+      __half v = __ushort_as_half(0x7C00);   // +inf: skipped (outside the image or all-NaN)
+      if (yy >= 0 && yy < A.H && xx >= 0 && xx < A.W) {
+        const size_t pi = s.pix0 + (size_t)yy * A.W + xx;
+        const uint8_t m = A.nan_map ? A.nan_map[pi] : 2;
+        const bool foot = yy >= s.ya - RHO && yy < s.yb + RHO;
+        if (foot && m == 3) partial = 1;
+        if (m != 1) v = __ushort2half_rn(A.guide[pi]);
+      }
+      gt[e] = v;
+    }
+    const bool clean = !__syncthreads_or(partial);
+    const int npass = clean ? 1 : 2;
+    if (warp >= n_cons) {
+      produce_weights<RHO>(A, g, s, clean, npass, gt, w_s, dpart, cost_s, full_w, empty_w, full_c, empty_c,
+                           it, it_c, warp - n_cons, lane);
+    } else {
+      const int t = tid;   // consumer thread: column t / G, lane-in-group t % G
       if (clean)
-        slide_consume<RHO, true>(c, warp);
+        consume<RHO, true>(A, g, s, cost_s, w_s, full_c, empty_c, full_w, empty_w, it, t / g.G, t % g.G, lane);
       else
-        slide_consume<RHO, false>(c, warp);
+        consume<RHO, false>(A, g, s, cost_s, w_s, full_c, empty_c, full_w, empty_w, it, t / g.G, t % g.G, lane);
     }
   }
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
 }
 
 template <int RHO>
 static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, float gamma_r,
                                   const float* vol, const uint8_t* guide, const uint8_t* nan_map,
                                   float* out, cudaStream_t st) {
-  const SlideGeom g = slide_geom(D, RHO, H);
+  const SlideGeom g = slide_geom(D, RHO);
   auto kern = k_aggregate_slide<RHO>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.bytes);
   if (e != cudaSuccess) { cudaGetLastError(); return e; }
+  SlideArgs A;
+  A.B = B; A.H = H; A.W = W; A.D = D;
+  const int nstrips = (W + 31) / 32;
+  const long long cols = (long long)nstrips * B * g.nslab;
+  // rows per CTA: minimise (waves of one-CTA-per-SM launches) x (rows + 2 rho warm-up)
+  const int nsm = sm_count();
+  int bestR = min(H, SG_SEGMAX);
+  double best = 1e300;
+  for (int n = (H + SG_SEGMAX - 1) / SG_SEGMAX; n <= H; n++) {
+    const int R = (H + n - 1) / n;
+    if (R < 8 && n > 1) break;
+    const long long ctas = cols * ((H + R - 1) / R);
+    const double cost = (double)((ctas + nsm - 1) / nsm) * (R + 2 * RHO);
+    if (cost < best * 0.999) { best = cost; bestR = R; }
+  }
+  A.R = bestR;
   const float log2e = 1.4426950408889634f;
-  const float kd = -log2e / (gamma_d * gamma_d);
-  const float kr = std::isinf(gamma_r) ? -1e-30f : -log2e / (gamma_r * gamma_r);
-  dim3 grid((W + 31) / 32, (H + g.R - 1) / g.R, B * g.nslab);
-  kern<<<grid, 32 * (((g.n_kg + 3) & ~3) + 4), g.bytes, st>>>(H, W, D, kd, kr, vol, guide, nan_map, out);
+  A.kd = -log2e / (gamma_d * gamma_d);
+  A.kr = std::isinf(gamma_r) ? -1e-30f : -log2e / (gamma_r * gamma_r);
+  A.vol = vol; A.guide = guide; A.nan_map = nan_map; A.out = out;
+  const dim3 grid(nstrips, (H + bestR - 1) / bestR, B * g.nslab);
+  kern<<<grid, 32 * (g.G + SG_NPROD), g.bytes, st>>>(A);
   return cudaGetLastError();
 }
 
-size_t aggregate_slide_smem(int D, int rho, int H) { return slide_geom(D, rho, H).bytes; }
+size_t aggregate_slide_smem(int D, int rho, int H) { (void)H; return slide_geom(D, rho).bytes; }
 
 cudaError_t launch_aggregate_slide(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r,
                                    const float* vol, const uint8_t* guide, const uint8_t* nan_map,

@@ -84,7 +84,7 @@ int rsr_aggregate(rsr_shape s, int32_t D, rsr_agg_params p, const float* vol, co
   if (!(p.gamma_d > 0.f) || std::isinf(p.gamma_d) || !(p.gamma_r > 0.f)) return RSR_E_ARG;
   if (vol == out) return RSR_E_ARG;
   if ((s.height + 7) / 8 > 65535) return RSR_E_ARG;
-  const long long nslab = (D + 127) / 128;
+  const long long nslab = (D + 63) / 64;
   if ((long long)s.batch * nslab > 65535) return RSR_E_ARG;
   return launched(rsr::launch_aggregate(s.batch, s.height, s.width, D, p.rho, p.gamma_d, p.gamma_r,
                                         vol, guide, nan_map, out, as_stream(stream)));

@@ -24,6 +24,14 @@ RSR_DEVINL float ex2_approx(float x) {
   return y;
 }
 
+// 2^x on the MUFU pipe, flushing subnormal results to 0 (one MUFU.EX2, no
+// range-reduction fix-up); exp2(-inf) = +0.
+RSR_DEVINL float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 RSR_DEVINL float qnan() { return __int_as_float(0x7fffffff); }
 
 // Clamp to [-1, 1] keeping NaN (fminf/fmaxf would drop it).
