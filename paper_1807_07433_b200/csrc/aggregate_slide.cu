@@ -101,6 +101,7 @@ struct Seg {
 struct SlideArgs {
   int B, H, W, D;
   int R;                 // output rows per CTA (<= SG_SEGMAX)
+  int nstrips;           // 32-column strips
   float kd, kr;
   const float* vol;
   const uint8_t* guide;
@@ -108,16 +109,24 @@ struct SlideArgs {
   float* out;
 };
 
-// The CTA's segment: blockIdx.x = strip, blockIdx.y = row chunk of R rows,
-// blockIdx.z = frame * nslab + slab.  The hardware block scheduler balances
-// clean and (twice as expensive) general-path segments across the SMs.
+// The CTA's segment.  The 1-D grid enumerates (strip rank, row chunk, frame x
+// slab) with the strip rank slowest and strips ranked 0, n-1, 1, n-2, ...:
+// image-edge strips, where stereo volumes hold partially-NaN pixels (the
+// general path, twice as expensive), launch first and the hardware block
+// scheduler back-fills the cheap interior strips (longest-first scheduling).
 RSR_DEVINL Seg cta_segment(const SlideArgs& A, const SlideGeom& g) {
   Seg s;
-  s.x0 = blockIdx.x * 32;
-  s.ya = blockIdx.y * A.R;
+  const int nchunk = (A.H + A.R - 1) / A.R;
+  const long long per_strip = (long long)nchunk * A.B * g.nslab;
+  const int rank = (int)(blockIdx.x / per_strip);
+  const int rest = (int)(blockIdx.x % per_strip);
+  const int strip = (rank & 1) ? A.nstrips - 1 - (rank >> 1) : (rank >> 1);
+  const int chunk = rest % nchunk, bz = rest / nchunk;
+  s.x0 = strip * 32;
+  s.ya = chunk * A.R;
   s.yb = min(A.H, s.ya + A.R);
-  s.b = blockIdx.z / g.nslab;
-  s.k0 = (blockIdx.z % g.nslab) * g.KS;
+  s.b = bz / g.nslab;
+  s.k0 = (bz % g.nslab) * g.KS;
   s.ks_eff = min(g.KS, A.D - s.k0);
   s.pix0 = (size_t)s.b * A.H * A.W;
   return s;
@@ -414,17 +423,31 @@ __global__ void __launch_bounds__(384, 1) k_aggregate_slide(const SlideArgs A) {
     // partially-NaN pixel (3) needs per-disparity denominators (the general path).
     int partial = (A.nan_map == nullptr) ? 1 : 0;
     const int rows = (s.yb - s.ya) + 4 * RHO;
-    for (int e = tid; e < rows * g.CX; e += blockDim.x) {
-      const int yy = s.ya - 2 * RHO + e / g.CX, xx = s.x0 - RHO + e % g.CX;
-      __half v = __ushort_as_half(0x7C00);   // +inf: skipped (outside the image or all-NaN)
-      if (yy >= 0 && yy < A.H && xx >= 0 && xx < A.W) {
-        const size_t pi = s.pix0 + (size_t)yy * A.W + xx;
-        const uint8_t m = A.nan_map ? A.nan_map[pi] : 2;
-        const bool foot = yy >= s.ya - RHO && yy < s.yb + RHO;
-        if (foot && m == 3) partial = 1;
-        if (m != 1) v = __ushort2half_rn(A.guide[pi]);
+    constexpr int UNR = 8;   // independent loads in flight per thread
+    for (int e0 = tid; e0 < rows * g.CX; e0 += UNR * blockDim.x) {
+      uint8_t mv[UNR], gv[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; u++) {
+        const int e = e0 + u * blockDim.x;
+        const int yy = s.ya - 2 * RHO + e / g.CX, xx = s.x0 - RHO + e % g.CX;
+        mv[u] = 1;   // outside the image: skipped like an all-NaN pixel
+        gv[u] = 0;
+        if (e < rows * g.CX && yy >= 0 && yy < A.H && xx >= 0 && xx < A.W) {
+          const size_t pi = s.pix0 + (size_t)yy * A.W + xx;
+          mv[u] = A.nan_map ? __ldg(A.nan_map + pi) : 2;
+          gv[u] = __ldg(A.guide + pi);
+        }
       }
-      gt[e] = v;
+#pragma unroll
+      for (int u = 0; u < UNR; u++) {
+        const int e = e0 + u * blockDim.x;
+        if (e < rows * g.CX) {
+          const int yy = s.ya - 2 * RHO + e / g.CX;
+          if (mv[u] == 3 && yy >= s.ya - RHO && yy < s.yb + RHO) partial = 1;
+          // +inf marks a skipped pixel (outside the image or all-NaN)
+          gt[e] = mv[u] == 1 ? __ushort_as_half(0x7C00) : __ushort2half_rn(gv[u]);
+        }
+      }
     }
     const bool clean = !__syncthreads_or(partial);
     const int npass = clean ? 1 : 2;
@@ -475,12 +498,14 @@ static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, flo
     if (cost < best * 0.999) { best = cost; bestR = R; }
   }
   A.R = bestR;
+  A.nstrips = nstrips;
   const float log2e = 1.4426950408889634f;
   A.kd = -log2e / (gamma_d * gamma_d);
   A.kr = std::isinf(gamma_r) ? -1e-30f : -log2e / (gamma_r * gamma_r);
   A.vol = vol; A.guide = guide; A.nan_map = nan_map; A.out = out;
-  const dim3 grid(nstrips, (H + bestR - 1) / bestR, B * g.nslab);
-  kern<<<grid, 32 * (g.G + SG_NPROD), g.bytes, st>>>(A);
+  const long long nblk = cols * ((H + bestR - 1) / bestR);
+  if (nblk > 0x7fffffffLL) return cudaErrorInvalidValue;
+  kern<<<(unsigned)nblk, 32 * (g.G + SG_NPROD), g.bytes, st>>>(A);
   return cudaGetLastError();
 }
 
