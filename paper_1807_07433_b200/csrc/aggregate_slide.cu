@@ -328,21 +328,23 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
           const float4 t = w4[q];
           wv[4 * q] = t.x; wv[4 * q + 1] = t.y; wv[4 * q + 2] = t.z; wv[4 * q + 3] = t.w;
         }
+        // q outer, ages inner: the cost pair stays in the operand reuse cache for
+        // 2 rho + 1 consecutive FFMA2s, so each reads only the weight and the
+        // accumulator pair from the register file (2 reads per bank)
         if (j < NT - 1) {
 #pragma unroll
-          for (int a = 0; a < NT; a++)
+          for (int q = 0; q < 4; q++)
 #pragma unroll
-            for (int q = 0; q < 4; q++) acc[a][q] = fma2s(wv[a], cp[q], acc[a][q]);
+            for (int a = 0; a < NT; a++) acc[a][q] = fma2s(wv[a], cp[q], acc[a][q]);
         } else {
           // last tap of the row: age 0 completes, every other age moves one slot down
 #pragma unroll
-          for (int q = 0; q < 4; q++) fin[q] = fma2s(wv[0], cp[q], acc[0][q]);
+          for (int q = 0; q < 4; q++) {
+            fin[q] = fma2s(wv[0], cp[q], acc[0][q]);
 #pragma unroll
-          for (int a = 1; a < NT; a++)
-#pragma unroll
-            for (int q = 0; q < 4; q++) acc[a - 1][q] = fma2s(wv[a], cp[q], acc[a][q]);
-#pragma unroll
-          for (int q = 0; q < 4; q++) acc[NT - 1][q] = make_float2(0.f, 0.f);
+            for (int a = 1; a < NT; a++) acc[a - 1][q] = fma2s(wv[a], cp[q], acc[a][q]);
+            acc[NT - 1][q] = make_float2(0.f, 0.f);
+          }
         }
       }
       const float den = CLEAN ? wrow[(32 - xl) * g.XS + xl] : 0.f;

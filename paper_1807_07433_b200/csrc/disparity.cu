@@ -14,24 +14,42 @@
 
 namespace rsr {
 
-// smallest index attaining the maximum over non-NaN entries; -1 if none.
-RSR_DEVINL int argmax_row(const float* __restrict__ p, int D, bool vec4) {
+// Group-cooperative argmax: G8 = 8 lanes own one pixel; lane l reads
+// disparities {4l..4l+3} and {32+4l..32+4l+3} of each 64-wide chunk (two
+// 16-byte loads; the 8 lanes of a group cover 256 contiguous bytes, a warp
+// four pixels = 1 KB per load pair), keeps the smallest index attaining the
+// maximum over non-NaN entries, and the group reduces (value, index) pairs
+// with three xor-shuffles.  -1 if no entry is finite.
+constexpr int DG = 8;   // lanes per pixel
+
+RSR_DEVINL void better(float v, int k, float& best, int& kb) {
+  // strictly greater, or equal with a smaller index (NaN never wins)
+  if (v > best || (v == best && k < kb && kb >= 0)) { best = v; kb = k; }
+}
+
+RSR_DEVINL int group_argmax(const float* __restrict__ p, int D, int l, bool vec4) {
   float best = -INFINITY;
   int kb = -1;
-  if (vec4) {
-    const float4* p4 = reinterpret_cast<const float4*>(p);
-    for (int k4 = 0; k4 < D / 4; k4++) {
-      const float4 t = __ldg(p4 + k4);
-      const float v[4] = {t.x, t.y, t.z, t.w};
+  for (int c0 = 0; c0 < D; c0 += 64) {
 #pragma unroll
-      for (int i = 0; i < 4; i++)
-        if (v[i] > best) { best = v[i]; kb = 4 * k4 + i; }  // NaN never compares greater
+    for (int h = 0; h < 2; h++) {
+      const int k = c0 + 32 * h + 4 * l;
+      if (vec4 && k + 3 < D) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(p + k));
+        better(t.x, k, best, kb); better(t.y, k + 1, best, kb);
+        better(t.z, k + 2, best, kb); better(t.w, k + 3, best, kb);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          if (k + q < D) better(__ldg(p + k + q), k + q, best, kb);
+      }
     }
-  } else {
-    for (int k = 0; k < D; k++) {
-      const float v = __ldg(p + k);
-      if (v > best) { best = v; kb = k; }
-    }
+  }
+#pragma unroll
+  for (int o = DG / 2; o >= 1; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int ok = __shfl_xor_sync(0xffffffffu, kb, o);
+    if (ok >= 0 && (kb < 0 || ov > best || (ov == best && ok < kb))) { best = ov; kb = ok; }
   }
   return kb;
 }
@@ -47,16 +65,23 @@ __global__ void __launch_bounds__(256) k_disparity(int H, int W, int d_lo, int D
   const int v = blockIdx.x, b = blockIdx.y;
   const size_t row = ((size_t)b * H + v) * W;
   const bool vec4 = (D & 3) == 0;
-  for (int u = threadIdx.x; u < W; u += blockDim.x) {
-    const int k = argmax_row(agg_tar + (row + u) * D, D, vec4);
-    kr_s[u] = (int16_t)k;
-    if (wta_tar) wta_tar[row + u] = (int16_t)k;
+  const int l = threadIdx.x % DG, g = threadIdx.x / DG, ng = blockDim.x / DG;
+  const int Wr = (W + ng - 1) / ng * ng;   // uniform trip count: every lane reaches the shuffles
+  for (int u = g; u < Wr; u += ng) {
+    const int uu = min(u, W - 1);
+    const int k = group_argmax(agg_tar + (row + uu) * D, D, l, vec4);
+    if (l == 0 && u < W) {
+      kr_s[u] = (int16_t)k;
+      if (wta_tar) wta_tar[row + u] = (int16_t)k;
+    }
   }
   __syncthreads();
   const float sv = (float)shift[(size_t)b * H + v];
-  for (int u = threadIdx.x; u < W; u += blockDim.x) {
-    const float* p = agg_ref + (row + u) * D;
-    const int k = argmax_row(p, D, vec4);
+  for (int u = g; u < Wr; u += ng) {
+    const int uu = min(u, W - 1);
+    const float* p = agg_ref + (row + uu) * D;
+    const int k = group_argmax(p, D, l, vec4);
+    if (l != 0 || u >= W) continue;
     if (wta_ref) wta_ref[row + u] = (int16_t)k;
     float d = qnan();
     if (k >= 0) {

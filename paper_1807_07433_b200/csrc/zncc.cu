@@ -47,12 +47,23 @@ __global__ void __launch_bounds__(256) k_block_stats(int H, int W, int p,
   int* cM = cSS + ST_TY * TC;
   const int b = blockIdx.z, x0 = blockIdx.x * ST_TX, y0 = blockIdx.y * ST_TY;
   const size_t base = (size_t)b * H * W;
-  for (int i = threadIdx.x; i < TR * TC; i += blockDim.x) {
-    const int yy = y0 - p + i / TC, xx = x0 - p + i % TC;
-    const bool in = yy >= 0 && yy < H && xx >= 0 && xx < W;
-    const size_t g = base + (size_t)yy * W + xx;
-    pix[i] = in ? (int)img[g] : 0;
-    msk[i] = in ? (mask ? (int)(mask[g] != 0) : 1) : 0;
+  constexpr int UNR = 8;   // independent loads in flight per thread
+  for (int i0 = threadIdx.x; i0 < TR * TC; i0 += UNR * blockDim.x) {
+    int pv[UNR], mv[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+      const int i = i0 + u * blockDim.x;
+      const int yy = y0 - p + i / TC, xx = x0 - p + i % TC;
+      const bool in = i < TR * TC && yy >= 0 && yy < H && xx >= 0 && xx < W;
+      const size_t g = base + (size_t)yy * W + xx;
+      pv[u] = in ? (int)__ldg(img + g) : 0;
+      mv[u] = in ? (mask ? (int)(__ldg(mask + g) != 0) : 1) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+      const int i = i0 + u * blockDim.x;
+      if (i < TR * TC) { pix[i] = pv[u]; msk[i] = mv[u]; }
+    }
   }
   __syncthreads();
   // vertical sliding sums, one column per thread
@@ -110,29 +121,42 @@ cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* im
 }
 
 // ---------------------------------------------------------------------------
-// NCC volume kernel
+// NCC volume kernel (streaming).  A CTA owns ZTX = 64 columns x all D (up to
+// 128) disparities and slides down ZBY rows.  Image rows and the block
+// statistics of the current output row stream through a small shared-memory
+// ring: every iteration first issues the global loads of the rows needed one
+// iteration later (kept in registers), computes the current row, then commits
+// the prefetched rows to the ring, so the load latency overlaps the math.
 // ---------------------------------------------------------------------------
 constexpr int ZX = 4;     // columns per thread
 constexpr int ZR = 8;     // disparities per thread
 constexpr int ZTX = 64;   // columns per CTA (16 column groups)
-constexpr int ZBY = 16;   // rows per CTA (vertical sliding band)
+constexpr int ZBY = 96;   // output rows per CTA
+constexpr int ZPF = 8;    // prefetch registers per thread per row
 
 struct ZnccGeom {
-  int FC, GC, SGC, gpad, NR;
+  int FC, GC, SGC, gpad, NRING, nload;
 };
 
 __host__ __device__ inline ZnccGeom zncc_geom(int p, int D) {
   ZnccGeom g;
-  g.NR = ZBY + 2 * p;
+  g.NRING = 2 * p + 2;                                   // image rows y-1 .. y+2p
   g.FC = ((ZTX + 2 * p + 3) / 4) * 4 + 4;
   g.gpad = (4 - (D & 3)) & 3;
   g.GC = ((ZTX + 2 * p + D - 1 + g.gpad + 3) / 4) * 4 + 8;
   g.SGC = ((ZTX + D - 1 + g.gpad + 3) / 4) * 4 + 8;
+  g.nload = g.FC + g.GC + 2 * ZTX + 2 * g.SGC;         // elements streamed per row
   return g;
 }
 
+__host__ __device__ inline size_t zncc_smem(int p, int D) {
+  const ZnccGeom g = zncc_geom(p, D);
+  return sizeof(float) * ((size_t)g.NRING * (g.FC + g.GC) + 2 * (2 * ZTX + 2 * (size_t)g.SGC)) +
+         sizeof(int) * (ZTX / ZX);
+}
+
 template <int P, bool TAR>
-__global__ void __launch_bounds__(256) k_zncc(int H, int W, int d_lo, int D, int Dst, int koff,
+__global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(int H, int W, int d_lo, int D, int Dst, int koff,
                                               bool nan_accumulate,
                                               const uint8_t* __restrict__ ref,
                                               const uint8_t* __restrict__ warped,
@@ -149,61 +173,108 @@ __global__ void __launch_bounds__(256) k_zncc(int H, int W, int d_lo, int D, int
   constexpr int NS4 = (SGR + 3) / 4;
   const ZnccGeom gm = zncc_geom(P, D);
   extern __shared__ __align__(16) float zsm[];
-  float* Fs = zsm;                          // [NR][FC]
-  float* Gs = Fs + gm.NR * gm.FC;           // [NR][GC]
-  float* sFs = Gs + gm.NR * gm.GC;          // [ZBY][ZTX]
-  float* iFs = sFs + ZBY * ZTX;             // [ZBY][ZTX]
-  float* sGs = iFs + ZBY * ZTX;             // [ZBY][SGC]
-  float* iGs = sGs + ZBY * gm.SGC;          // [ZBY][SGC]
-  int* flags = reinterpret_cast<int*>(iGs + ZBY * gm.SGC);  // [ZBY][ZTX]
+  float* Fs = zsm;                                  // [NRING][FC]  image rows, F side
+  float* Gs = Fs + gm.NRING * gm.FC;                // [NRING][GC]  image rows, G side
+  float* St = Gs + gm.NRING * gm.GC;                // [2][sF ZTX | iF ZTX | sG SGC | iG SGC]
+  int* flags = reinterpret_cast<int*>(St + 2 * (2 * ZTX + 2 * gm.SGC));  // [ZTX/ZX] 4 x 2 bits
+  const int SROW = 2 * ZTX + 2 * gm.SGC;
 
   const int b = blockIdx.z, x0 = blockIdx.x * ZTX, y0 = blockIdx.y * ZBY;
   const int d_hi = d_lo + D - 1;
   const size_t ibase = (size_t)b * H * W;
-  // F = image at the fixed column; G = image at the shifted column x + sg*r.
+  // F = image at the fixed column; G = image at the shifted column x -/+ r.
   const uint8_t* Fimg = TAR ? warped : ref;
   const uint8_t* Gimg = TAR ? ref : warped;
   const int32_t* SFg = TAR ? SWg : SLg;
   const float* iFg = TAR ? invWg : invLg;
   const int32_t* SGg = TAR ? SLg : SWg;
   const float* iGg = TAR ? invLg : invWg;
-  // first image column held in Gs / sGs
+  // first image column held in Gs / the G statistics
   const int g0 = TAR ? (x0 - P + d_lo) : (x0 - P - d_hi - gm.gpad);
   const int s0 = TAR ? (x0 + d_lo) : (x0 - d_hi - gm.gpad);
+  const int nrows = min(ZBY, H - y0);
 
-  for (int i = threadIdx.x; i < gm.NR * gm.FC; i += blockDim.x) {
-    const int yy = y0 - P + i / gm.FC, xx = x0 - P + i % gm.FC;
-    Fs[i] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? (float)Fimg[ibase + (size_t)yy * W + xx] : 0.f;
+  // ---- row streaming: element e of the row-t load list -> (smem slot, value) ----
+  // image row t (absolute y0 - P + t) feeds ring slot t % NRING; the statistics of
+  // output row y feed St[y & 1].
+  // Loads land in raw registers (image byte, int32 sum or fp32 inverse norm) and are
+  // converted only at commit time, one iteration later, so no instruction waits on
+  // them inside the iteration that issued them.
+  constexpr int NPI = 2, NPS = 4;   // image / statistics elements per thread per row
+  uint32_t pi_[NPI], ps_[NPS];
+  const int NIMG = gm.FC + gm.GC, NSTAT = 2 * ZTX + 2 * gm.SGC;
+  auto fetch = [&](int t_img, int y_st) {
+    const int yy_i = y0 - P + t_img, yy_s = y0 + y_st;
+    const bool row_i = t_img >= 0 && yy_i >= 0 && yy_i < H;
+#pragma unroll
+    for (int u = 0; u < NPI; u++) {
+      const int e = threadIdx.x + u * 128;
+      const bool isF = e < gm.FC;
+      const int xx = isF ? x0 - P + e : g0 + (e - gm.FC);
+      const uint8_t* img = isF ? Fimg : Gimg;
+      pi_[u] = (row_i && e < NIMG && xx >= 0 && xx < W) ? (uint32_t)__ldg(img + ibase + (size_t)yy_i * W + xx) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < NPS; u++) {
+      const int k = threadIdx.x + u * 128;
+      uint32_t v = 0u;
+      if (y_st >= 0 && k < NSTAT) {
+        const bool isF = k < 2 * ZTX;
+        const int kk = isF ? k : k - 2 * ZTX;
+        const int per = isF ? ZTX : gm.SGC;
+        const bool isInv = kk >= per;
+        const int xx = (isF ? x0 : s0) + (isInv ? kk - per : kk);
+        const bool in = yy_s < H && xx >= 0 && xx < W;
+        const size_t gi = ibase + (size_t)yy_s * W + xx;
+        if (isInv) v = in ? __float_as_uint(__ldg((isF ? iFg : iGg) + gi)) : 0x7fffffffu;
+        else v = in ? (uint32_t)__ldg((isF ? SFg : SGg) + gi) : 0u;
+      }
+      ps_[u] = v;
+    }
+  };
+  // exact integer -> float for 0 <= v < 2^23 without the XU pipe
+  auto u2f = [](uint32_t v) { return __uint_as_float(0x4B000000u | v) - 8388608.0f; };
+  auto commit = [&](int t_img, int y_st) {
+    const int slot = t_img % gm.NRING;
+    if (t_img >= 0) {
+#pragma unroll
+      for (int u = 0; u < NPI; u++) {
+        const int e = threadIdx.x + u * 128;
+        if (e < gm.FC) Fs[slot * gm.FC + e] = u2f(pi_[u]);
+        else if (e < NIMG) Gs[slot * gm.GC + (e - gm.FC)] = u2f(pi_[u]);
+      }
+    }
+    if (y_st >= 0) {
+      float* st = St + (y_st & 1) * SROW;
+#pragma unroll
+      for (int u = 0; u < NPS; u++) {
+        const int k = threadIdx.x + u * 128;
+        if (k < NSTAT) {
+          const bool isF = k < 2 * ZTX;
+          const int kk = isF ? k : k - 2 * ZTX;
+          const bool isInv = kk >= (isF ? ZTX : gm.SGC);
+          st[k] = isInv ? __uint_as_float(ps_[u]) : u2f(ps_[u]);
+        }
+      }
+    }
+  };
+
+  // prologue: image rows 0 .. 2P and the statistics of output row 0
+  for (int t = 0; t <= 2 * P; t++) {
+    fetch(t, t == 0 ? 0 : -1);
+    commit(t, t == 0 ? 0 : -1);
   }
-  for (int i = threadIdx.x; i < gm.NR * gm.GC; i += blockDim.x) {
-    const int yy = y0 - P + i / gm.GC, xx = g0 + i % gm.GC;
-    Gs[i] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? (float)Gimg[ibase + (size_t)yy * W + xx] : 0.f;
-  }
-  for (int i = threadIdx.x; i < ZBY * ZTX; i += blockDim.x) {
-    const int yy = y0 + i / ZTX, xx = x0 + i % ZTX;
-    const bool in = yy < H && xx < W;
-    sFs[i] = in ? (float)SFg[ibase + (size_t)yy * W + xx] : 0.f;
-    iFs[i] = in ? iFg[ibase + (size_t)yy * W + xx] : qnan();
-    flags[i] = 0;
-  }
-  for (int i = threadIdx.x; i < ZBY * gm.SGC; i += blockDim.x) {
-    const int yy = y0 + i / gm.SGC, xx = s0 + i % gm.SGC;
-    const bool in = yy < H && xx >= 0 && xx < W;
-    sGs[i] = in ? (float)SGg[ibase + (size_t)yy * W + xx] : 0.f;
-    iGs[i] = in ? iGg[ibase + (size_t)yy * W + xx] : qnan();
-  }
+  if (threadIdx.x < ZTX / ZX) flags[threadIdx.x] = 0;
   __syncthreads();
 
   const int n_rg = (D + ZR - 1) / ZR;
   const int rg = threadIdx.x % n_rg, cg = threadIdx.x / n_rg;
-  if (cg >= ZTX / ZX) return;
+  const bool active = cg < ZTX / ZX;
   const int r0 = d_lo + ZR * rg;               // first residual disparity of the thread
   const int u_t = x0 + ZX * cg;                // first column of the thread
-  // run starts (element index in the smem row)
-  const int f_start = ZX * cg;                                  // column u_t - P
-  const int g_start = TAR ? (ZX * cg + ZR * rg)                 // column u_t - P + r0
-                          : (ZX * cg + D - ZR - ZR * rg + gm.gpad);  // column u_t - P - r0 - 7
-  const int sg_start = TAR ? (ZX * cg + ZR * rg) : (ZX * cg + D - ZR - ZR * rg + gm.gpad);
+  const int f_start = ZX * cg;                 // column u_t - P
+  const int g_start = TAR ? (ZX * cg + ZR * rg) : (ZX * cg + D - ZR - ZR * rg + gm.gpad);
+  const int sg_start = g_start;
   const float nf = (float)((2 * P + 1) * (2 * P + 1));
 
   float V[NJ][ZR];
@@ -212,19 +283,20 @@ __global__ void __launch_bounds__(256) k_zncc(int H, int W, int d_lo, int D, int
 #pragma unroll
     for (int q = 0; q < ZR; q++) V[j][q] = 0.f;
 
-  auto accumulate_row = [&](int srow, float sign) {
+  auto accumulate_row = [&](int t, float sign) {
+    const int slot = t % gm.NRING;
     float f[NF4 * 4], g[NG4 * 4];
-    const float4* fr = reinterpret_cast<const float4*>(Fs + srow * gm.FC + f_start);
-    const float4* gr = reinterpret_cast<const float4*>(Gs + srow * gm.GC + g_start);
+    const float4* fr = reinterpret_cast<const float4*>(Fs + slot * gm.FC + f_start);
+    const float4* gr = reinterpret_cast<const float4*>(Gs + slot * gm.GC + g_start);
 #pragma unroll
     for (int i = 0; i < NF4; i++) {
-      const float4 t = fr[i];
-      f[4 * i] = t.x; f[4 * i + 1] = t.y; f[4 * i + 2] = t.z; f[4 * i + 3] = t.w;
+      const float4 v = fr[i];
+      f[4 * i] = v.x; f[4 * i + 1] = v.y; f[4 * i + 2] = v.z; f[4 * i + 3] = v.w;
     }
 #pragma unroll
     for (int i = 0; i < NG4; i++) {
-      const float4 t = gr[i];
-      g[4 * i] = t.x; g[4 * i + 1] = t.y; g[4 * i + 2] = t.z; g[4 * i + 3] = t.w;
+      const float4 v = gr[i];
+      g[4 * i] = v.x; g[4 * i + 1] = v.y; g[4 * i + 2] = v.z; g[4 * i + 3] = v.w;
     }
 #pragma unroll
     for (int j = 0; j < NJ; j++) {
@@ -232,88 +304,108 @@ __global__ void __launch_bounds__(256) k_zncc(int H, int W, int d_lo, int D, int
 #pragma unroll
       for (int q = 0; q < ZR; q++) {
         const int m = TAR ? (j + q) : (j - q + ZR - 1);
-        V[j][q] = fmaf(fj, g[m], V[j][q]);
+        V[j][q] = fmaf(fj, g[m], V[j][q]);   // exact: integer products and sums < 2^24
       }
     }
   };
 
-  const int nrows = min(ZBY, H - y0);
   for (int y = 0; y < nrows; y++) {
-    if (y == 0) {
+    // prefetch image row y + 1 + 2P and the statistics of output row y + 1
+    const bool more = y + 1 < nrows;
+    if (more) fetch(y + 1 + 2 * P, y + 1);
+    if (active) {
+      if (y == 0) {
 #pragma unroll 1
-      for (int dy = 0; dy < 2 * P + 1; dy++) accumulate_row(dy, 1.f);
-    } else {
-      accumulate_row(y + 2 * P, 1.f);
-      accumulate_row(y - 1, -1.f);
-    }
-    // block statistics of this row
-    float sF[ZX], iF[ZX], sG[NS4 * 4], iG[NS4 * 4];
-    {
-      const float4 a = *reinterpret_cast<const float4*>(sFs + y * ZTX + ZX * cg);
-      const float4 c = *reinterpret_cast<const float4*>(iFs + y * ZTX + ZX * cg);
-      sF[0] = a.x; sF[1] = a.y; sF[2] = a.z; sF[3] = a.w;
-      iF[0] = c.x; iF[1] = c.y; iF[2] = c.z; iF[3] = c.w;
-      const float4* sr = reinterpret_cast<const float4*>(sGs + y * gm.SGC + sg_start);
-      const float4* ir = reinterpret_cast<const float4*>(iGs + y * gm.SGC + sg_start);
-#pragma unroll
-      for (int i = 0; i < NS4; i++) {
-        const float4 t = sr[i], u = ir[i];
-        sG[4 * i] = t.x; sG[4 * i + 1] = t.y; sG[4 * i + 2] = t.z; sG[4 * i + 3] = t.w;
-        iG[4 * i] = u.x; iG[4 * i + 1] = u.y; iG[4 * i + 2] = u.z; iG[4 * i + 3] = u.w;
+        for (int t = 0; t <= 2 * P; t++) accumulate_row(t, 1.f);
+      } else {
+        accumulate_row(y + 2 * P, 1.f);
+        accumulate_row(y - 1, -1.f);
       }
-    }
-    const int yy = y0 + y;
-    float* vrow = vol + ((ibase + (size_t)yy * W) * Dst) + koff;
+      // block statistics of this row
+      const float* st = St + (y & 1) * SROW;
+      float sF[ZX], iF[ZX], sG[NS4 * 4], iG[NS4 * 4];
+      {
+        const float4 a = *reinterpret_cast<const float4*>(st + ZX * cg);
+        const float4 c = *reinterpret_cast<const float4*>(st + ZTX + ZX * cg);
+        sF[0] = a.x; sF[1] = a.y; sF[2] = a.z; sF[3] = a.w;
+        iF[0] = c.x; iF[1] = c.y; iF[2] = c.z; iF[3] = c.w;
+        const float4* sr = reinterpret_cast<const float4*>(st + 2 * ZTX + sg_start);
+        const float4* ir = reinterpret_cast<const float4*>(st + 2 * ZTX + gm.SGC + sg_start);
 #pragma unroll
-    for (int i = 0; i < ZX; i++) {
-      const int u = u_t + i;
-      float out[ZR];
-      bool anynan = false, anyfin = false;
+        for (int i = 0; i < NS4; i++) {
+          const float4 t = sr[i], u = ir[i];
+          sG[4 * i] = t.x; sG[4 * i + 1] = t.y; sG[4 * i + 2] = t.z; sG[4 * i + 3] = t.w;
+          iG[4 * i] = u.x; iG[4 * i + 1] = u.y; iG[4 * i + 2] = u.z; iG[4 * i + 3] = u.w;
+        }
+      }
+      const int yy = y0 + y;
+      float* vrow = vol + ((ibase + (size_t)yy * W) * Dst) + koff;
+      int fl4 = 0;
+      float s = 0.f;   // sliding horizontal (2P+1)-sum, per disparity
+      float hs[ZR];
 #pragma unroll
       for (int q = 0; q < ZR; q++) {
-        float s = 0.f;
+        float a = 0.f;
 #pragma unroll
-        for (int dx = 0; dx < 2 * P + 1; dx++) s += V[i + dx][q];
-        const int m = TAR ? (i + q) : (i - q + ZR - 1);
-        // left block = L at u_left, right block = W at u_left - r
-        const float sL = TAR ? sG[m] : sF[i];
-        const float sR = TAR ? sF[i] : sG[m];
-        const float iL = TAR ? iG[m] : iF[i];
-        const float iR = TAR ? iF[i] : iG[m];
-        const float a = nf * s;
-        const float ae = fmaf(nf, s, -a);
-        const float bb = sL * sR;
-        const float be = fmaf(sL, sR, -bb);
-        const float num = (a - bb) + (ae - be);
-        const float c = clamp_unit_keep_nan((num * iL) * iR);
-        out[q] = c;
-        anynan |= (r0 + q <= d_hi) && (c != c);
-        anyfin |= (r0 + q <= d_hi) && (c == c);
+        for (int dx = 0; dx < 2 * P + 1; dx++) a += V[dx][q];
+        hs[q] = a;
       }
-      if (u < W) {
-        float* dst = vrow + (size_t)u * Dst + (r0 - d_lo);
-        if ((Dst & 3) == 0 && (koff & 3) == 0 && r0 + ZR - 1 <= d_hi) {
-          reinterpret_cast<float4*>(dst)[0] = make_float4(out[0], out[1], out[2], out[3]);
-          reinterpret_cast<float4*>(dst)[1] = make_float4(out[4], out[5], out[6], out[7]);
-        } else {
 #pragma unroll
-          for (int q = 0; q < ZR; q++)
-            if (r0 + q <= d_hi) dst[q] = out[q];
+      for (int i = 0; i < ZX; i++) {
+        const int u = u_t + i;
+        float out[ZR];
+        bool anynan = false, anyfin = false;
+#pragma unroll
+        for (int q = 0; q < ZR; q++) {
+          if (i > 0) hs[q] = (hs[q] + V[i + 2 * P][q]) - V[i - 1][q];   // exact integers
+          s = hs[q];
+          const int m = TAR ? (i + q) : (i - q + ZR - 1);
+          // left block = L at u_left, right block = W at u_left - r
+          const float sL = TAR ? sG[m] : sF[i];
+          const float sR = TAR ? sF[i] : sG[m];
+          const float iL = TAR ? iG[m] : iF[i];
+          const float iR = TAR ? iF[i] : iG[m];
+          const float a = nf * s;
+          const float ae = fmaf(nf, s, -a);
+          const float bb = sL * sR;
+          const float be = fmaf(sL, sR, -bb);
+          const float num = (a - bb) + (ae - be);
+          const float c = clamp_unit_keep_nan((num * iL) * iR);
+          out[q] = c;
+          anynan |= (r0 + q <= d_hi) && (c != c);
+          anyfin |= (r0 + q <= d_hi) && (c == c);
         }
-        const int fl = (anynan ? 1 : 0) | (anyfin ? 2 : 0);
-        if (fl && nan_map) atomicOr(&flags[y * ZTX + ZX * cg + i], fl);
+        if (u < W) {
+          float* dst = vrow + (size_t)u * Dst + (r0 - d_lo);
+          if ((Dst & 3) == 0 && (koff & 3) == 0 && r0 + ZR - 1 <= d_hi) {
+            reinterpret_cast<float4*>(dst)[0] = make_float4(out[0], out[1], out[2], out[3]);
+            reinterpret_cast<float4*>(dst)[1] = make_float4(out[4], out[5], out[6], out[7]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < ZR; q++)
+              if (r0 + q <= d_hi) dst[q] = out[q];
+          }
+        }
+        fl4 |= ((anynan ? 1 : 0) | (anyfin ? 2 : 0)) << (8 * i);
+      }
+      if (nan_map && fl4) atomicOr(&flags[cg], fl4);
+    }
+    __syncthreads();   // ring slot of row y - 1 and St[(y + 1) & 1] are free; flags complete
+    if (nan_map && threadIdx.x < ZTX / ZX) {
+      const int fl4 = flags[threadIdx.x];
+      flags[threadIdx.x] = 0;
+      const int yy = y0 + y;
+#pragma unroll
+      for (int i = 0; i < ZX; i++) {
+        const int xx = x0 + ZX * threadIdx.x + i;
+        if (xx < W) {
+          uint8_t* mp = nan_map + ibase + (size_t)yy * W + xx;
+          *mp = (uint8_t)(((fl4 >> (8 * i)) & 3) | (nan_accumulate ? *mp : 0));
+        }
       }
     }
-  }
-  if (nan_map) {
+    if (more) commit(y + 1 + 2 * P, y + 1);
     __syncthreads();
-    for (int i = threadIdx.x; i < ZBY * ZTX; i += blockDim.x) {
-      const int yy = y0 + i / ZTX, xx = x0 + i % ZTX;
-      if (yy < H && xx < W) {
-        uint8_t* m = nan_map + ibase + (size_t)yy * W + xx;
-        *m = (uint8_t)(flags[i] | (nan_accumulate ? *m : 0));
-      }
-    }
   }
 }
 
@@ -323,15 +415,14 @@ static cudaError_t zncc_launch_t(int B, int H, int W, int d_lo, int D, int Dst, 
                                  const uint8_t* warped, const int32_t* SL, const float* invL,
                                  const int32_t* SW, const float* invW, float* vol,
                                  uint8_t* nan_map, cudaStream_t st) {
-  const ZnccGeom gm = zncc_geom(P, D);
-  const size_t smem = sizeof(float) * ((size_t)gm.NR * gm.FC + (size_t)gm.NR * gm.GC +
-                                       2 * ZBY * ZTX + 2 * (size_t)ZBY * gm.SGC) +
-                      sizeof(int) * ZBY * ZTX;
+  const size_t smem = zncc_smem(P, D);
   auto kern = k_zncc<P, TAR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) { cudaGetLastError(); return e; }
-  const int n_rg = (D + ZR - 1) / ZR;
-  const int threads = n_rg * (ZTX / ZX);
+  // always 128 threads: (D <= 64) / 8 disparity groups x 16 column groups compute,
+  // and all of them stream the rows (ZPF x 128 >= the longest row load list)
+  const int threads = 128;
+  static_assert(2 * 128 >= 84 + 152 && 4 * 128 >= 2 * ZTX + 2 * 136, "row load lists must fit the prefetch");
   // threads > 1024 is rejected by the API (D > 512 would need a k-slab split)
   dim3 grid((W + ZTX - 1) / ZTX, (H + ZBY - 1) / ZBY, B);
   kern<<<grid, threads, smem, st>>>(H, W, d_lo, D, Dst, koff, nan_acc, ref, warped, SL, invL, SW,
@@ -343,9 +434,9 @@ cudaError_t launch_zncc(bool tar, int B, int H, int W, int rho_b, int d_lo, int 
                         const uint8_t* ref, const uint8_t* warped, const int32_t* SL,
                         const float* invL, const int32_t* SW, const float* invW, float* vol,
                         uint8_t* nan_map, cudaStream_t st) {
-  // Disparity slabs of at most 128 (<= 256 threads per CTA); later slabs OR
+  // Disparity slabs of at most 64 (<= 128 threads per CTA); later slabs OR
   // their NaN flags into the map written by the first.
-  constexpr int SLAB = 128;
+  constexpr int SLAB = 64;
   for (int k0 = 0; k0 < D; k0 += SLAB) {
     const int Ds = D - k0 < SLAB ? D - k0 : SLAB;
     const int dl = d_lo + k0;

@@ -49,5 +49,8 @@ def bench(B, H, W, D, rho, nan_frac_cols=0.0, reps=5, gamma_d=4.0, gamma_r=12.0)
 if __name__ == "__main__":
     cases = [(8, 720, 1280, 64, 6, 0.0), (8, 720, 1280, 64, 6, 0.1), (1, 720, 1280, 64, 6, 0.0),
              (8, 720, 1280, 64, 4, 0.0), (2, 1080, 1920, 96, 7, 0.0), (8, 360, 640, 48, 5, 0.0)]
+    if len(sys.argv) > 1:   # one case: B H W D rho nan_band [reps]
+        a = sys.argv[1:]
+        cases = [(int(a[0]), int(a[1]), int(a[2]), int(a[3]), int(a[4]), float(a[5]))]
     for c in cases:
-        print(json.dumps(bench(*c)), flush=True)
+        print(json.dumps(bench(*c, reps=int(os.environ.get("REPS", "5")))), flush=True)

@@ -1,0 +1,174 @@
+// K3 inner-loop variants: how the shared-memory operand loads interact with the
+// FFMA2 stream (13 ages x 4 cost pairs per tap, 2 warps per SMSP).
+//   mode 0: costs 2 x LDS.128, weights 4 x LDS.128 (current K3)
+//   mode 1: weights 13 x LDS.32
+//   mode 2: weights 7 x LDS.64
+//   mode 3: explicit double buffer (tap j+1 operands loaded before tap j FFMA2s)
+//   mode 4: costs 4 x LDS.64
+//   mode 5: mode 3 with a-outer order
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ float2 fma2s(float w, float2 c, float2 a) {
+  unsigned long long av, cv, wb, dv;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(av) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(cv) : "f"(c.x), "f"(c.y));
+  asm("mov.b64 %0, {%1,%1};" : "=l"(wb) : "f"(w));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(dv) : "l"(wb), "l"(cv), "l"(av));
+  float2 d;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(dv));
+  return d;
+}
+
+template <int MODE>
+__device__ __forceinline__ void load_tap(const float* cb, const float* wb, int j, int it, float (&wv)[16], float2 (&cp)[4]) {
+  const int co = (j * 64 + it * 4) & 511;
+  if (MODE == 4) {
+    const float2 c0 = *reinterpret_cast<const float2*>(cb + co), c1 = *reinterpret_cast<const float2*>(cb + co + 2);
+    const float2 c2 = *reinterpret_cast<const float2*>(cb + co + 32), c3 = *reinterpret_cast<const float2*>(cb + co + 34);
+    cp[0] = c0; cp[1] = c1; cp[2] = c2; cp[3] = c3;
+  } else {
+    const float4 ca = *reinterpret_cast<const float4*>(cb + co);
+    const float4 cc = *reinterpret_cast<const float4*>(cb + co + 32);
+    cp[0] = make_float2(ca.x, ca.y); cp[1] = make_float2(ca.z, ca.w);
+    cp[2] = make_float2(cc.x, cc.y); cp[3] = make_float2(cc.z, cc.w);
+  }
+  const float* w = wb + ((j * 16 + it * 4) & 1023);
+  if (MODE == 1) {
+#pragma unroll
+    for (int a = 0; a < 13; a++) wv[a] = w[a];
+  } else if (MODE == 2) {
+#pragma unroll
+    for (int a = 0; a < 14; a += 2) { float2 t = *reinterpret_cast<const float2*>(w + a); wv[a] = t.x; wv[a + 1] = t.y; }
+  } else {
+    const float4* w4 = reinterpret_cast<const float4*>(w);
+#pragma unroll
+    for (int q = 0; q < 3; q++) { float4 t = w4[q]; wv[4*q]=t.x; wv[4*q+1]=t.y; wv[4*q+2]=t.z; wv[4*q+3]=t.w; }
+    wv[12] = w[12];
+  }
+}
+
+template <int MODE>
+__global__ void k(float* out, int iters) {
+  __shared__ __align__(16) float sm[4096];
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) sm[i] = 1e-3f * (i & 63);
+  __syncthreads();
+  float2 acc[13][4];
+#pragma unroll
+  for (int a = 0; a < 13; a++)
+#pragma unroll
+    for (int q = 0; q < 4; q++) acc[a][q] = make_float2(0.f, 0.f);
+  const int lane = threadIdx.x & 31;
+  const float* cb = sm + (lane & 7) * 4;
+  const float* wb = sm + 1024 + (lane >> 3) * 20;
+  for (int it = 0; it < iters; it++) {
+    if (MODE == 3 || MODE == 5) {
+      float wv[2][16]; float2 cp[2][4];
+      load_tap<0>(cb, wb, 0, it, wv[0], cp[0]);
+#pragma unroll
+      for (int j = 0; j < 13; j++) {
+        if (j + 1 < 13) load_tap<0>(cb, wb, j + 1, it, wv[(j + 1) & 1], cp[(j + 1) & 1]);
+        if (MODE == 3) {
+#pragma unroll
+          for (int q = 0; q < 4; q++)
+#pragma unroll
+            for (int a = 0; a < 13; a++) acc[a][q] = fma2s(wv[j & 1][a], cp[j & 1][q], acc[a][q]);
+        } else {
+#pragma unroll
+          for (int a = 0; a < 13; a++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) acc[a][q] = fma2s(wv[j & 1][a], cp[j & 1][q], acc[a][q]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 13; j++) {
+        float wv[16]; float2 cp[4];
+        load_tap<MODE>(cb, wb, j, it, wv, cp);
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+#pragma unroll
+          for (int a = 0; a < 13; a++) acc[a][q] = fma2s(wv[a], cp[q], acc[a][q]);
+      }
+    }
+  }
+  float s = 0;
+#pragma unroll
+  for (int a = 0; a < 13; a++)
+#pragma unroll
+    for (int q = 0; q < 4; q++) s += acc[a][q].x + acc[a][q].y;
+  if (s == 12345.f) out[threadIdx.x] = s;
+}
+
+// K_l = 4 variant: 13 ages x 2 cost pairs per tap (52 accumulator registers), so
+// 3-4 warps fit per SMSP
+template <int NA>
+__global__ void k4(float* out, int iters) {
+  __shared__ __align__(16) float sm[4096];
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) sm[i] = 1e-3f * (i & 63);
+  __syncthreads();
+  float2 acc[NA][2];
+#pragma unroll
+  for (int a = 0; a < NA; a++) { acc[a][0] = make_float2(0.f, 0.f); acc[a][1] = acc[a][0]; }
+  const int lane = threadIdx.x & 31;
+  const float* cb = sm + (lane & 15) * 4;
+  const float* wb = sm + 1024 + (lane >> 4) * 20;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int j = 0; j < 13; j++) {
+      const float4 ca = *reinterpret_cast<const float4*>(cb + ((j * 64 + it * 4) & 511));
+      float2 cp[2] = {make_float2(ca.x, ca.y), make_float2(ca.z, ca.w)};
+      const float* w = wb + ((j * 16 + it * 4) & 1023);
+      float wv[16];
+      const float4* w4 = reinterpret_cast<const float4*>(w);
+#pragma unroll
+      for (int q = 0; q < (NA + 3) / 4; q++) { float4 t = w4[q]; wv[4*q]=t.x; wv[4*q+1]=t.y; wv[4*q+2]=t.z; wv[4*q+3]=t.w; }
+#pragma unroll
+      for (int q = 0; q < 2; q++)
+#pragma unroll
+        for (int a = 0; a < NA; a++) acc[a][q] = fma2s(wv[a], cp[q], acc[a][q]);
+    }
+  }
+  float s = 0;
+#pragma unroll
+  for (int a = 0; a < NA; a++) s += acc[a][0].x + acc[a][0].y + acc[a][1].x + acc[a][1].y;
+  if (s == 12345.f) out[threadIdx.x] = s;
+}
+
+int main() {
+  float* out; cudaMalloc(&out, 1 << 16);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  int sms = 148;
+  for (int wps = 1; wps <= 4; wps++) {
+    int threads = 128 * wps, iters = 2000;
+    auto launch = [&] { k4<13><<<sms, threads>>>(out, iters); };
+    launch(); cudaDeviceSynchronize();
+    float best = 1e30f;
+    for (int r = 0; r < 5; r++) { cudaEventRecord(e0); launch(); cudaEventRecord(e1); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1); if (ms < best) best = ms; }
+    double flop = 2.0 * sms * threads * (double)iters * 13 * 13 * 4;
+    printf("{\"mode\": \"kl4\", \"warps_per_smsp\": %d, \"ms\": %.3f, \"frac_of_74.45\": %.3f, \"err\": \"%s\"}\n", wps, best,
+           flop / best / 1e9 / 74.45, cudaGetErrorString(cudaGetLastError()));
+  }
+  for (int mode = 0; mode < 1; mode++)
+    for (int wps = 1; wps <= 2; wps++) {
+      int threads = 128 * wps, iters = 2000;
+      auto launch = [&] {
+        switch (mode) {
+          case 0: k<0><<<sms, threads>>>(out, iters); break;
+          case 1: k<1><<<sms, threads>>>(out, iters); break;
+          case 2: k<2><<<sms, threads>>>(out, iters); break;
+          case 3: k<3><<<sms, threads>>>(out, iters); break;
+          case 4: k<4><<<sms, threads>>>(out, iters); break;
+          default: k<5><<<sms, threads>>>(out, iters); break;
+        }
+      };
+      launch(); cudaDeviceSynchronize();
+      float best = 1e30f;
+      for (int r = 0; r < 5; r++) { cudaEventRecord(e0); launch(); cudaEventRecord(e1); cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1); if (ms < best) best = ms; }
+      double flop = 2.0 * sms * threads * (double)iters * 13 * 13 * 8;
+      printf("{\"mode\": %d, \"warps_per_smsp\": %d, \"ms\": %.3f, \"frac_of_74.45\": %.3f, \"err\": \"%s\"}\n", mode, wps, best,
+             flop / best / 1e9 / 74.45, cudaGetErrorString(cudaGetLastError()));
+    }
+}
