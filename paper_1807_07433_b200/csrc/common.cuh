@@ -32,6 +32,47 @@ RSR_DEVINL float ex2_ftz(float x) {
   return y;
 }
 
+// Packed fp32x2 arithmetic (FFMA2 / FMUL2 family), element-wise.
+RSR_DEVINL unsigned long long f2pack(float2 v) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+RSR_DEVINL float2 f2unpack(unsigned long long r) {
+  float2 v;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+RSR_DEVINL float2 f2fma(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2pack(a)), "l"(f2pack(b)), "l"(f2pack(c)));
+  return f2unpack(d);
+}
+RSR_DEVINL float2 f2mul(float2 a, float2 b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2pack(a)), "l"(f2pack(b)));
+  return f2unpack(d);
+}
+
+RSR_DEVINL float2 f2add(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2pack(a)), "l"(f2pack(b)));
+  return f2unpack(d);
+}
+RSR_DEVINL float2 f2sub(float2 a, float2 b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2pack(a)), "l"(f2pack(b)));
+  return f2unpack(d);
+}
+
+// Clamp to [-1, 1], propagating NaN (max.NaN / min.NaN: one FMNMX each).
+RSR_DEVINL float clamp_unit_nan(float c) {
+  float t, r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(t) : "f"(c), "f"(-1.f));
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(t), "f"(1.f));
+  return r;
+}
+
 RSR_DEVINL float qnan() { return __int_as_float(0x7fffffff); }
 
 // Clamp to [-1, 1] keeping NaN (fminf/fmaxf would drop it).

@@ -129,29 +129,40 @@ cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* im
 // the prefetched rows to the ring, so the load latency overlaps the math.
 // ---------------------------------------------------------------------------
 constexpr int ZX = 4;     // columns per thread
-constexpr int ZR = 8;     // disparities per thread
+constexpr int ZR = 8;     // disparities per thread (4 packed pairs)
 constexpr int ZTX = 64;   // columns per CTA (16 column groups)
 constexpr int ZBY = 96;   // output rows per CTA
-constexpr int ZPF = 8;    // prefetch registers per thread per row
 
+// Shared-memory rows are stored "oriented": the G-side image row and G-side
+// statistics run so that, for a thread, the G entry of disparity q + 1 follows
+// the one of disparity q (reference volume: G = W at u - r, stored reversed;
+// target volume: G = L at u' + r, stored forward).  Each oriented row also has
+// a copy shifted by one entry, so that a (q, q+1) pair starting at an odd
+// index is still an aligned register pair: every packed operand is one LDS.
 struct ZnccGeom {
-  int FC, GC, SGC, gpad, NRING, nload;
+  int FC, GC, SGC, gpad, NRING, GROW, SROW2, RB, RS;
 };
 
 __host__ __device__ inline ZnccGeom zncc_geom(int p, int D) {
   ZnccGeom g;
+  const int NJ = ZX + 2 * p;
   g.NRING = 2 * p + 2;                                   // image rows y-1 .. y+2p
   g.FC = ((ZTX + 2 * p + 3) / 4) * 4 + 4;
   g.gpad = (4 - (D & 3)) & 3;
   g.GC = ((ZTX + 2 * p + D - 1 + g.gpad + 3) / 4) * 4 + 8;
   g.SGC = ((ZTX + D - 1 + g.gpad + 3) / 4) * 4 + 8;
-  g.nload = g.FC + g.GC + 2 * ZTX + 2 * g.SGC;         // elements streamed per row
+  // reversal origins (reference volume), chosen so the thread runs stay 16-byte aligned
+  g.RB = g.GC - 1 + ((NJ + 6 - (g.GC - 1)) & 3);
+  g.RS = g.SGC - 1 + ((ZX + ZR - 2 - (g.SGC - 1)) & 3);
+  g.GROW = g.GC + 8;                                     // oriented G image row (+ shifted copy)
+  g.SROW2 = g.SGC + 8;                                   // oriented G statistics row
   return g;
 }
 
 __host__ __device__ inline size_t zncc_smem(int p, int D) {
   const ZnccGeom g = zncc_geom(p, D);
-  return sizeof(float) * ((size_t)g.NRING * (g.FC + g.GC) + 2 * (2 * ZTX + 2 * (size_t)g.SGC)) +
+  // ring: F rows, oriented G rows x2; statistics double buffer: sF, iF, sG x2, iG x2
+  return sizeof(float) * ((size_t)g.NRING * (g.FC + 2 * g.GROW) + 2 * (2 * ZTX + 4 * (size_t)g.SROW2)) +
          sizeof(int) * (ZTX / ZX);
 }
 
@@ -167,17 +178,19 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
                                               float* __restrict__ vol,
                                               uint8_t* __restrict__ nan_map) {
   constexpr int NJ = ZX + 2 * P;          // V columns per thread
-  constexpr int NG = ZX + 2 * P + ZR - 1; // G run length
-  constexpr int NF4 = (NJ + 3) / 4, NG4 = (NG + 3) / 4;
-  constexpr int SGR = ZX + ZR - 1;        // G-stats run length
-  constexpr int NS4 = (SGR + 3) / 4;
+  constexpr int NQP = ZR / 2;             // disparity pairs per thread
+  constexpr int NGR = NJ + ZR;            // oriented G run loaded per row (>= NJ + ZR - 1)
+  constexpr int NF4 = (NJ + 3) / 4, NG4 = (NGR + 3) / 4;
+  constexpr int NSR = ZX + ZR;            // oriented G-statistics run (>= ZX + ZR - 1)
+  constexpr int NS4 = (NSR + 3) / 4;
   const ZnccGeom gm = zncc_geom(P, D);
   extern __shared__ __align__(16) float zsm[];
-  float* Fs = zsm;                                  // [NRING][FC]  image rows, F side
-  float* Gs = Fs + gm.NRING * gm.FC;                // [NRING][GC]  image rows, G side
-  float* St = Gs + gm.NRING * gm.GC;                // [2][sF ZTX | iF ZTX | sG SGC | iG SGC]
-  int* flags = reinterpret_cast<int*>(St + 2 * (2 * ZTX + 2 * gm.SGC));  // [ZTX/ZX] 4 x 2 bits
-  const int SROW = 2 * ZTX + 2 * gm.SGC;
+  float* Fs = zsm;                                   // [NRING][FC]    F image rows
+  float* Gs = Fs + gm.NRING * gm.FC;                 // [NRING][GROW]  oriented G image rows
+  float* Gs1 = Gs + gm.NRING * gm.GROW;              // [NRING][GROW]  shifted by one entry
+  float* St = Gs1 + gm.NRING * gm.GROW;              // [2][sF ZTX | iF ZTX | sG | sG1 | iG | iG1]
+  int* flags = reinterpret_cast<int*>(St + 2 * (2 * ZTX + 4 * gm.SROW2));  // [ZTX/ZX] 4 x 2 bits
+  const int SROW = 2 * ZTX + 4 * gm.SROW2;
 
   const int b = blockIdx.z, x0 = blockIdx.x * ZTX, y0 = blockIdx.y * ZBY;
   const int d_hi = d_lo + D - 1;
@@ -189,17 +202,15 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
   const float* iFg = TAR ? invWg : invLg;
   const int32_t* SGg = TAR ? SLg : SWg;
   const float* iGg = TAR ? invLg : invWg;
-  // first image column held in Gs / the G statistics
+  // first image column of the (unoriented) G image row / G statistics row
   const int g0 = TAR ? (x0 - P + d_lo) : (x0 - P - d_hi - gm.gpad);
   const int s0 = TAR ? (x0 + d_lo) : (x0 - d_hi - gm.gpad);
   const int nrows = min(ZBY, H - y0);
+  // unoriented index c -> oriented index
+  auto orient_g = [&](int c) { return TAR ? c : gm.RB - c; };
+  auto orient_s = [&](int c) { return TAR ? c : gm.RS - c; };
 
-  // ---- row streaming: element e of the row-t load list -> (smem slot, value) ----
-  // image row t (absolute y0 - P + t) feeds ring slot t % NRING; the statistics of
-  // output row y feed St[y & 1].
-  // Loads land in raw registers (image byte, int32 sum or fp32 inverse norm) and are
-  // converted only at commit time, one iteration later, so no instruction waits on
-  // them inside the iteration that issued them.
+  // ---- row streaming (loads land raw in registers, converted one iteration later) ----
   constexpr int NPI = 2, NPS = 4;   // image / statistics elements per thread per row
   uint32_t pi_[NPI], ps_[NPS];
   const int NIMG = gm.FC + gm.GC, NSTAT = 2 * ZTX + 2 * gm.SGC;
@@ -240,8 +251,14 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
 #pragma unroll
       for (int u = 0; u < NPI; u++) {
         const int e = threadIdx.x + u * 128;
-        if (e < gm.FC) Fs[slot * gm.FC + e] = u2f(pi_[u]);
-        else if (e < NIMG) Gs[slot * gm.GC + (e - gm.FC)] = u2f(pi_[u]);
+        if (e < gm.FC) {
+          Fs[slot * gm.FC + e] = u2f(pi_[u]);
+        } else if (e < NIMG) {
+          const int o = orient_g(e - gm.FC);
+          const float v = u2f(pi_[u]);
+          Gs[slot * gm.GROW + o] = v;
+          if (o > 0) Gs1[slot * gm.GROW + o - 1] = v;
+        }
       }
     }
     if (y_st >= 0) {
@@ -249,11 +266,16 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
 #pragma unroll
       for (int u = 0; u < NPS; u++) {
         const int k = threadIdx.x + u * 128;
-        if (k < NSTAT) {
-          const bool isF = k < 2 * ZTX;
-          const int kk = isF ? k : k - 2 * ZTX;
-          const bool isInv = kk >= (isF ? ZTX : gm.SGC);
-          st[k] = isInv ? __uint_as_float(ps_[u]) : u2f(ps_[u]);
+        if (k < 2 * ZTX) {
+          st[k] = k >= ZTX ? __uint_as_float(ps_[u]) : u2f(ps_[u]);
+        } else if (k < NSTAT) {
+          const int kk = k - 2 * ZTX;
+          const bool isInv = kk >= gm.SGC;
+          const float v = isInv ? __uint_as_float(ps_[u]) : u2f(ps_[u]);
+          const int o = orient_s(isInv ? kk - gm.SGC : kk);
+          float* row = st + 2 * ZTX + (isInv ? 2 : 0) * gm.SROW2;   // sG | sG1 | iG | iG1
+          row[o] = v;
+          if (o > 0) row[gm.SROW2 + o - 1] = v;
         }
       }
     }
@@ -274,20 +296,25 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
   const int u_t = x0 + ZX * cg;                // first column of the thread
   const int f_start = ZX * cg;                 // column u_t - P
   const int g_start = TAR ? (ZX * cg + ZR * rg) : (ZX * cg + D - ZR - ZR * rg + gm.gpad);
-  const int sg_start = g_start;
+  // oriented run starts (16-byte aligned): entry of (j, q) = run + j * dj + q
+  const int grun = TAR ? g_start : gm.RB - g_start - (NJ - 1) - (ZR - 1);
+  const int srun = TAR ? g_start : gm.RS - g_start - (ZX - 1) - (ZR - 1);
   const float nf = (float)((2 * P + 1) * (2 * P + 1));
 
-  float V[NJ][ZR];
+  // V2[j][qp] = sum over the 2P+1 block rows of F(col j) * (G(q), G(q+1)) for q = 2qp:
+  // exact integers < 2^24 accumulated by FFMA2 with the F value as scalar operand.
+  float2 V2[NJ][NQP];
 #pragma unroll
   for (int j = 0; j < NJ; j++)
 #pragma unroll
-    for (int q = 0; q < ZR; q++) V[j][q] = 0.f;
+    for (int qp = 0; qp < NQP; qp++) V2[j][qp] = make_float2(0.f, 0.f);
 
-  auto accumulate_row = [&](int t, float sign) {
+  auto accumulate_row = [&](int t, bool subtract) {
     const int slot = t % gm.NRING;
-    float f[NF4 * 4], g[NG4 * 4];
+    float f[NF4 * 4], ge[NG4 * 4], go[NG4 * 4];
     const float4* fr = reinterpret_cast<const float4*>(Fs + slot * gm.FC + f_start);
-    const float4* gr = reinterpret_cast<const float4*>(Gs + slot * gm.GC + g_start);
+    const float4* gr = reinterpret_cast<const float4*>(Gs + slot * gm.GROW + grun);
+    const float4* gr1 = reinterpret_cast<const float4*>(Gs1 + slot * gm.GROW + grun);
 #pragma unroll
     for (int i = 0; i < NF4; i++) {
       const float4 v = fr[i];
@@ -295,16 +322,20 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
     }
 #pragma unroll
     for (int i = 0; i < NG4; i++) {
-      const float4 v = gr[i];
-      g[4 * i] = v.x; g[4 * i + 1] = v.y; g[4 * i + 2] = v.z; g[4 * i + 3] = v.w;
+      const float4 v = gr[i], w = gr1[i];
+      ge[4 * i] = v.x; ge[4 * i + 1] = v.y; ge[4 * i + 2] = v.z; ge[4 * i + 3] = v.w;
+      go[4 * i] = w.x; go[4 * i + 1] = w.y; go[4 * i + 2] = w.z; go[4 * i + 3] = w.w;
     }
 #pragma unroll
     for (int j = 0; j < NJ; j++) {
-      const float fj = sign * f[j];
+      const float fj = subtract ? -f[j] : f[j];
+      // oriented offset of (j, q = 0): TAR j, REF (NJ - 1) - j
+      const int o0 = TAR ? j : (NJ - 1 - j);
 #pragma unroll
-      for (int q = 0; q < ZR; q++) {
-        const int m = TAR ? (j + q) : (j - q + ZR - 1);
-        V[j][q] = fmaf(fj, g[m], V[j][q]);   // exact: integer products and sums < 2^24
+      for (int qp = 0; qp < NQP; qp++) {
+        const int o = o0 + 2 * qp;
+        const float2 gp = (o & 1) ? make_float2(go[o - 1], go[o]) : make_float2(ge[o], ge[o + 1]);
+        V2[j][qp] = f2fma(make_float2(fj, fj), gp, V2[j][qp]);
       }
     }
   };
@@ -316,76 +347,93 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
     if (active) {
       if (y == 0) {
 #pragma unroll 1
-        for (int t = 0; t <= 2 * P; t++) accumulate_row(t, 1.f);
+        for (int t = 0; t <= 2 * P; t++) accumulate_row(t, false);
       } else {
-        accumulate_row(y + 2 * P, 1.f);
-        accumulate_row(y - 1, -1.f);
+        accumulate_row(y + 2 * P, false);
+        accumulate_row(y - 1, true);
       }
-      // block statistics of this row
+      // block statistics of this row: F side per pixel, G side as oriented pairs
       const float* st = St + (y & 1) * SROW;
-      float sF[ZX], iF[ZX], sG[NS4 * 4], iG[NS4 * 4];
+      float sF[ZX], iF[ZX], sGe[NS4 * 4], sGo[NS4 * 4], iGe[NS4 * 4], iGo[NS4 * 4];
       {
         const float4 a = *reinterpret_cast<const float4*>(st + ZX * cg);
         const float4 c = *reinterpret_cast<const float4*>(st + ZTX + ZX * cg);
         sF[0] = a.x; sF[1] = a.y; sF[2] = a.z; sF[3] = a.w;
         iF[0] = c.x; iF[1] = c.y; iF[2] = c.z; iF[3] = c.w;
-        const float4* sr = reinterpret_cast<const float4*>(st + 2 * ZTX + sg_start);
-        const float4* ir = reinterpret_cast<const float4*>(st + 2 * ZTX + gm.SGC + sg_start);
+        const float* sg = st + 2 * ZTX + srun;
 #pragma unroll
         for (int i = 0; i < NS4; i++) {
-          const float4 t = sr[i], u = ir[i];
-          sG[4 * i] = t.x; sG[4 * i + 1] = t.y; sG[4 * i + 2] = t.z; sG[4 * i + 3] = t.w;
-          iG[4 * i] = u.x; iG[4 * i + 1] = u.y; iG[4 * i + 2] = u.z; iG[4 * i + 3] = u.w;
+          const float4 t0 = reinterpret_cast<const float4*>(sg)[i];
+          const float4 t1 = reinterpret_cast<const float4*>(sg + gm.SROW2)[i];
+          const float4 t2 = reinterpret_cast<const float4*>(sg + 2 * gm.SROW2)[i];
+          const float4 t3 = reinterpret_cast<const float4*>(sg + 3 * gm.SROW2)[i];
+          sGe[4 * i] = t0.x; sGe[4 * i + 1] = t0.y; sGe[4 * i + 2] = t0.z; sGe[4 * i + 3] = t0.w;
+          sGo[4 * i] = t1.x; sGo[4 * i + 1] = t1.y; sGo[4 * i + 2] = t1.z; sGo[4 * i + 3] = t1.w;
+          iGe[4 * i] = t2.x; iGe[4 * i + 1] = t2.y; iGe[4 * i + 2] = t2.z; iGe[4 * i + 3] = t2.w;
+          iGo[4 * i] = t3.x; iGo[4 * i + 1] = t3.y; iGo[4 * i + 2] = t3.z; iGo[4 * i + 3] = t3.w;
         }
       }
       const int yy = y0 + y;
       float* vrow = vol + ((ibase + (size_t)yy * W) * Dst) + koff;
+      // NaN structure from the statistics alone (num is always finite): c(i, q) is NaN
+      // iff iF[i] or the G-side norm of (i, q) is NaN; over q those are the oriented
+      // entries [oi, oi + ZR) with oi = TAR ? i : ZX - 1 - i.
+      uint32_t gnan = 0;
+#pragma unroll
+      for (int m = 0; m < ZX + ZR - 1; m++) gnan |= (iGe[m] != iGe[m] ? 1u : 0u) << m;
+      const int nq = min(ZR, d_hi - r0 + 1);   // disparities of this thread inside the slab
+      const uint32_t qmask = nq >= ZR ? 0xFFu : ((1u << max(nq, 0)) - 1u);
       int fl4 = 0;
-      float s = 0.f;   // sliding horizontal (2P+1)-sum, per disparity
-      float hs[ZR];
+      float2 hs[NQP];
 #pragma unroll
-      for (int q = 0; q < ZR; q++) {
-        float a = 0.f;
+      for (int qp = 0; qp < NQP; qp++) {
+        float2 acc = V2[0][qp];
 #pragma unroll
-        for (int dx = 0; dx < 2 * P + 1; dx++) a += V[dx][q];
-        hs[q] = a;
+        for (int dx = 1; dx < 2 * P + 1; dx++) acc = f2add(acc, V2[dx][qp]);
+        hs[qp] = acc;
       }
 #pragma unroll
       for (int i = 0; i < ZX; i++) {
         const int u = u_t + i;
-        float out[ZR];
-        bool anynan = false, anyfin = false;
+        if (i > 0) {
 #pragma unroll
-        for (int q = 0; q < ZR; q++) {
-          if (i > 0) hs[q] = (hs[q] + V[i + 2 * P][q]) - V[i - 1][q];   // exact integers
-          s = hs[q];
-          const int m = TAR ? (i + q) : (i - q + ZR - 1);
-          // left block = L at u_left, right block = W at u_left - r
-          const float sL = TAR ? sG[m] : sF[i];
-          const float sR = TAR ? sF[i] : sG[m];
-          const float iL = TAR ? iG[m] : iF[i];
-          const float iR = TAR ? iF[i] : iG[m];
-          const float a = nf * s;
-          const float ae = fmaf(nf, s, -a);
-          const float bb = sL * sR;
-          const float be = fmaf(sL, sR, -bb);
-          const float num = (a - bb) + (ae - be);
-          const float c = clamp_unit_keep_nan((num * iL) * iR);
-          out[q] = c;
-          anynan |= (r0 + q <= d_hi) && (c != c);
-          anyfin |= (r0 + q <= d_hi) && (c == c);
+          for (int qp = 0; qp < NQP; qp++)   // sliding horizontal sum, exact integers
+            hs[qp] = f2sub(f2add(hs[qp], V2[i + 2 * P][qp]), V2[i - 1][qp]);
+        }
+        const int oi = TAR ? i : (ZX - 1 - i);
+        float2 out[NQP];
+#pragma unroll
+        for (int qp = 0; qp < NQP; qp++) {
+          const int o = oi + 2 * qp;
+          const float2 sg = (o & 1) ? make_float2(sGo[o - 1], sGo[o]) : make_float2(sGe[o], sGe[o + 1]);
+          const float2 ig = (o & 1) ? make_float2(iGo[o - 1], iGo[o]) : make_float2(iGe[o], iGe[o + 1]);
+          const float2 sf = make_float2(sF[i], sF[i]), inf = make_float2(iF[i], iF[i]);
+          const float2 nn = make_float2(nf, nf);
+          // n S_lw - S_l S_w with error-free products (cancellation-safe)
+          const float2 a = f2mul(nn, hs[qp]);
+          const float2 ae = f2fma(nn, hs[qp], make_float2(-a.x, -a.y));
+          const float2 bb = f2mul(sf, sg);
+          const float2 be = f2fma(sf, sg, make_float2(-bb.x, -bb.y));
+          const float2 num = f2add(f2sub(a, bb), f2sub(ae, be));
+          // (num * inv_L) * inv_W, in this order for both volumes (bitwise dual identity)
+          const float2 c = TAR ? f2mul(f2mul(num, ig), inf) : f2mul(f2mul(num, inf), ig);
+          out[qp] = make_float2(clamp_unit_nan(c.x), clamp_unit_nan(c.y));
         }
         if (u < W) {
           float* dst = vrow + (size_t)u * Dst + (r0 - d_lo);
-          if ((Dst & 3) == 0 && (koff & 3) == 0 && r0 + ZR - 1 <= d_hi) {
-            reinterpret_cast<float4*>(dst)[0] = make_float4(out[0], out[1], out[2], out[3]);
-            reinterpret_cast<float4*>(dst)[1] = make_float4(out[4], out[5], out[6], out[7]);
+          if ((Dst & 3) == 0 && (koff & 3) == 0 && nq >= ZR) {
+            reinterpret_cast<float4*>(dst)[0] = make_float4(out[0].x, out[0].y, out[1].x, out[1].y);
+            reinterpret_cast<float4*>(dst)[1] = make_float4(out[2].x, out[2].y, out[3].x, out[3].y);
           } else {
 #pragma unroll
             for (int q = 0; q < ZR; q++)
-              if (r0 + q <= d_hi) dst[q] = out[q];
+              if (q < nq) dst[q] = (q & 1) ? out[q >> 1].y : out[q >> 1].x;
           }
         }
+        const bool fnan = iF[i] != iF[i];
+        const uint32_t win = (gnan >> oi) & qmask;   // oriented: entry oi + q <-> disparity q
+        const bool anynan = nq > 0 && (fnan || win != 0);
+        const bool anyfin = nq > 0 && !fnan && win != qmask;
         fl4 |= ((anynan ? 1 : 0) | (anyfin ? 2 : 0)) << (8 * i);
       }
       if (nan_map && fl4) atomicOr(&flags[cg], fl4);
