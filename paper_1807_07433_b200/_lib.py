@@ -8,7 +8,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librsr.so")
+# RSR_LIB selects an alternative in-tree build (A/B experiments under tools/)
+LIB_PATH = os.environ.get("RSR_LIB") or os.path.join(HERE, "librsr.so")
 
 RSR_OK, RSR_E_ARG, RSR_E_DATA, RSR_E_INTERNAL = 0, 2, 3, 4
 

@@ -23,7 +23,16 @@ def up_to_date():
     return all(os.path.getmtime(d) <= t for d in deps)
 
 
-def build(force=False, verbose=False):
+def build(force=False, verbose=False, out=None, defines=()):
+    """Compile every csrc/*.cu into one shared library (default: librsr.so)."""
+    if out is not None:   # experiment build (tools/): always rebuilt
+        cmd = [os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")] + NVCC_FLAGS + \
+              ["-D" + d for d in defines] + ["-o", out] + sources()
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stderr)
+            raise RuntimeError("nvcc failed")
+        return out
     if not force and up_to_date():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -50,7 +50,7 @@ constexpr int SG_SEGMAX = 720;  // max output rows per segment (guide tile heigh
 
 struct SlideGeom {
   int G, KS, nslab, CX, XS, WST, GR;
-  size_t off_cost, off_w, off_dpart, off_guide, off_bar, bytes;
+  size_t off_cost, off_w, off_dpart, off_guide, off_tapf, off_bar, bytes;
 };
 
 // KS = disparities per slab (multiple of 8, <= 64), G = consumer lanes per column
@@ -70,6 +70,8 @@ __host__ __device__ inline SlideGeom slide_geom(int D, int rho) {
   g.off_w = o;     o += sizeof(float) * (size_t)SG_NSW * g.WST;
   g.off_dpart = o; o += sizeof(float) * (size_t)NT * 32;
   g.off_guide = o; o += sizeof(__half) * (size_t)g.GR * g.CX;
+  o = (o + 15) & ~size_t(15);
+  g.off_tapf = o;  o += sizeof(float) * 2 * (size_t)g.CX;
   o = (o + 15) & ~size_t(15);
   g.off_bar = o;   o += 8 * (2 * SG_NSC + 2 * SG_NSW);
   g.bytes = o;
@@ -206,7 +208,7 @@ __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g
 template <int RHO>
 __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideGeom& g, const Seg& s,
                                                 bool clean, int npass, const __half* gt, float* w_s,
-                                                float* dsum, float* cost_s, uint64_t* full_w,
+                                                float* dsum, float* tapf, float* cost_s, uint64_t* full_w,
                                                 uint64_t* empty_w, uint64_t* full_c, uint64_t* empty_c,
                                                 uint32_t& it_w, uint32_t& it_c, int p, int lane) {
   constexpr int NT = 2 * RHO + 1;
@@ -215,13 +217,15 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
   const int xs = lane >> 2, as = lane & 3;
   for (int pass = 0; pass < npass; pass++) {
     for (int e = p * 32 + lane; e < NT * 32; e += SG_NPROD * 32) dsum[e] = 0.f;
+    // tap row 0 as float (the tile is fp16; converting once per row instead of once per weight)
+    for (int c = p * 32 + lane; c < g.CX; c += SG_NPROD * 32) tapf[c] = __half2float(gt[RHO * g.CX + c]);
     asm volatile("bar.sync 1, %0;" ::"r"(SG_NPROD * 32) : "memory");
     for (int i = 0; i < NR; i++, it_w++) {
       if (p == 0) stage_row<RHO>(A, g, s, clean, i, gt, cost_s, full_c, empty_c, it_c, lane);
       const int st = it_w % SG_NSW;
       if (it_w >= SG_NSW) mbar_wait_parity(&empty_w[st], ((it_w / SG_NSW) & 1) ^ 1);
       float* wst = w_s + (size_t)st * g.WST;
-      const __half* trow = gt + (i + RHO) * g.CX;   // tap row r
+      const float* trow = tapf + (i & 1) * g.CX;   // tap row r (tile row i + RHO) as float
       // this warp's items (x-block, age-block) = p + 4 n, n < NAB; all shared-memory
       // loads first, then the math, then the stores: the tile, the running sums and
       // the weight stage may alias as far as the compiler knows, so interleaving them
@@ -240,7 +244,7 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
         gp[n] = isinf(cg) ? -cg : cg;
         den[n] = dsum[((i + a) % NT) * 32 + x];
 #pragma unroll
-        for (int j = 0; j < NT; j++) wv[n][j] = __half2float(trow[x + j]);
+        for (int j = 0; j < NT; j++) wv[n][j] = (float)trow[x + j];
       }
 #pragma unroll
       for (int n = 0; n < NAB; n++) {
@@ -272,6 +276,11 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
           }
         }
       }
+      // next tap row as float into the other buffer (its last readers finished before
+      // the previous barrier)
+      if (i + 1 < NR)
+        for (int c = p * 32 + lane; c < g.CX; c += SG_NPROD * 32)
+          tapf[((i + 1) & 1) * g.CX + c] = __half2float(gt[(i + 1 + RHO) * g.CX + c]);
       asm volatile("bar.sync 1, %0;" ::"r"(SG_NPROD * 32) : "memory");   // row sums handed to the next age
       mbar_arrive(&full_w[st]);
     }
@@ -399,6 +408,7 @@ __global__ void __launch_bounds__(384, 1) k_aggregate_slide(const SlideArgs A) {
   float* w_s = reinterpret_cast<float*>(sl_smem + g.off_w);
   float* dpart = reinterpret_cast<float*>(sl_smem + g.off_dpart);
   __half* gt = reinterpret_cast<__half*>(sl_smem + g.off_guide);
+  float* tapf = reinterpret_cast<float*>(sl_smem + g.off_tapf);
   uint64_t* full_c = reinterpret_cast<uint64_t*>(sl_smem + g.off_bar);
   uint64_t* empty_c = full_c + SG_NSC;
   uint64_t* full_w = empty_c + SG_NSC;
@@ -454,7 +464,7 @@ __global__ void __launch_bounds__(384, 1) k_aggregate_slide(const SlideArgs A) {
     const bool clean = !__syncthreads_or(partial);
     const int npass = clean ? 1 : 2;
     if (warp >= n_cons) {
-      produce_weights<RHO>(A, g, s, clean, npass, gt, w_s, dpart, cost_s, full_w, empty_w, full_c, empty_c,
+      produce_weights<RHO>(A, g, s, clean, npass, gt, w_s, dpart, tapf, cost_s, full_w, empty_w, full_c, empty_c,
                            it, it_c, warp - n_cons, lane);
     } else {
       const int t = tid;   // consumer thread: column t / G, lane-in-group t % G

@@ -217,10 +217,9 @@ def test_nan_map_optional_same_within_tolerance(rsr):
     a = run_gpu(rsr, f.left, f.right, [f.alpha, f.beta], cfg, nan_maps=True)
     b = run_gpu(rsr, f.left, f.right, [f.alpha, f.beta], cfg, nan_maps=False)
     for key in ("agg_ref", "agg_tar"):
-        x, y = a[key], b[key]
-        assert np.array_equal(np.isnan(x), np.isnan(y))
-        m = ~np.isnan(x)
-        assert np.abs(x[m] - y[m]).max() <= 1e-5
+        # the clean path (nan_map) and the general path accumulate in the same order:
+        # bitwise equal (aggregate_slide.cu, "produce_weights")
+        assert np.array_equal(a[key], b[key], equal_nan=True), key
 
 
 def test_determinism_and_batch_independence(rsr):

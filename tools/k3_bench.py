@@ -15,7 +15,7 @@ import paper_1807_07433_b200 as rsr  # noqa: E402
 FP32_PEAK = 148 * 128 * 2 * 1.965e9
 
 
-def bench(B, H, W, D, rho, nan_frac_cols=0.0, reps=5, gamma_d=4.0, gamma_r=12.0):
+def bench(B, H, W, D, rho, nan_frac_cols=0.0, reps=5, gamma_d=4.0, gamma_r=12.0, ws="auto"):
     g = torch.Generator(device="cuda").manual_seed(0)
     vol = torch.rand((B, H, W, D), device="cuda", generator=g) * 2 - 1
     nan_map = torch.full((B, H, W), 2, dtype=torch.uint8, device="cuda")
@@ -42,7 +42,7 @@ def bench(B, H, W, D, rho, nan_frac_cols=0.0, reps=5, gamma_d=4.0, gamma_r=12.0)
         ts.append(e0.elapsed_time(e1))
     ms = min(ts)
     flop = 2.0 * B * H * W * D * (2 * rho + 1) ** 2
-    return {"B": B, "H": H, "W": W, "D": D, "rho": rho, "nan_band": nan_frac_cols, "ms": ms,
+    return {"lib": os.path.basename(rsr._lib.LIB_PATH), "B": B, "H": H, "W": W, "D": D, "rho": rho, "nan_band": nan_frac_cols, "ms": ms,
             "tflops": flop / ms / 1e9, "frac": flop / (ms * 1e-3) / FP32_PEAK}
 
 
