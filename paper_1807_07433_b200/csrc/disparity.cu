@@ -22,29 +22,41 @@ namespace rsr {
 // with three xor-shuffles.  -1 if no entry is finite.
 constexpr int DG = 8;   // lanes per pixel
 
-RSR_DEVINL void better(float v, int k, float& best, int& kb) {
-  // strictly greater, or equal with a smaller index (NaN never wins)
-  if (v > best || (v == best && k < kb && kb >= 0)) { best = v; kb = k; }
-}
-
-RSR_DEVINL int group_argmax(const float* __restrict__ p, int D, int l, bool vec4) {
-  float best = -INFINITY;
-  int kb = -1;
+// Lane-local part: the lane's best over its 8 entries of each 64-wide chunk.  A
+// lane sees its disparities in increasing order, so "strictly greater" keeps the
+// first (smallest) index among equal maxima; max(x, NaN) = x skips NaN entries.
+// Per 8 values: 8 FMNMX for the maximum, then the first index equal to it.
+RSR_DEVINL void lane_best(const float* __restrict__ p, int D, int l, bool vec4, float& best, int& kb) {
+  best = -INFINITY;
+  kb = -1;
   for (int c0 = 0; c0 < D; c0 += 64) {
+    float v[8];
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       const int k = c0 + 32 * h + 4 * l;
       if (vec4 && k + 3 < D) {
         const float4 t = __ldg(reinterpret_cast<const float4*>(p + k));
-        better(t.x, k, best, kb); better(t.y, k + 1, best, kb);
-        better(t.z, k + 2, best, kb); better(t.w, k + 3, best, kb);
+        v[4 * h] = t.x; v[4 * h + 1] = t.y; v[4 * h + 2] = t.z; v[4 * h + 3] = t.w;
       } else {
 #pragma unroll
-        for (int q = 0; q < 4; q++)
-          if (k + q < D) better(__ldg(p + k + q), k + q, best, kb);
+        for (int q = 0; q < 4; q++) v[4 * h + q] = (k + q < D) ? __ldg(p + k + q) : qnan();
       }
     }
+    float m = v[0];
+#pragma unroll
+    for (int q = 1; q < 8; q++) m = fmaxf(m, v[q]);
+    if (m > best) {   // false when every entry is NaN (m is NaN)
+      best = m;
+      int kk = -1;
+#pragma unroll
+      for (int q = 7; q >= 0; q--)
+        if (v[q] == m) kk = c0 + 32 * (q >> 2) + 4 * l + (q & 3);
+      kb = kk;
+    }
   }
+}
+
+RSR_DEVINL int group_reduce(float best, int kb) {
 #pragma unroll
   for (int o = DG / 2; o >= 1; o >>= 1) {
     const float ov = __shfl_xor_sync(0xffffffffu, best, o);
@@ -52,6 +64,13 @@ RSR_DEVINL int group_argmax(const float* __restrict__ p, int D, int l, bool vec4
     if (ok >= 0 && (kb < 0 || ov > best || (ov == best && ok < kb))) { best = ov; kb = ok; }
   }
   return kb;
+}
+
+RSR_DEVINL int group_argmax(const float* __restrict__ p, int D, int l, bool vec4) {
+  float best;
+  int kb;
+  lane_best(p, D, l, vec4, best, kb);
+  return group_reduce(best, kb);
 }
 
 __global__ void __launch_bounds__(256) k_disparity(int H, int W, int d_lo, int D, int tol,
@@ -66,40 +85,62 @@ __global__ void __launch_bounds__(256) k_disparity(int H, int W, int d_lo, int D
   const size_t row = ((size_t)b * H + v) * W;
   const bool vec4 = (D & 3) == 0;
   const int l = threadIdx.x % DG, g = threadIdx.x / DG, ng = blockDim.x / DG;
-  const int Wr = (W + ng - 1) / ng * ng;   // uniform trip count: every lane reaches the shuffles
-  for (int u = g; u < Wr; u += ng) {
-    const int uu = min(u, W - 1);
-    const int k = group_argmax(agg_tar + (row + uu) * D, D, l, vec4);
-    if (l == 0 && u < W) {
-      kr_s[u] = (int16_t)k;
-      if (wta_tar) wta_tar[row + u] = (int16_t)k;
+  const int Wr = (W + 4 * ng - 1) / (4 * ng) * (4 * ng);   // uniform trip count: every lane reaches the shuffles
+  // four pixels per group per iteration: eight 16-byte loads in flight per lane
+  constexpr int UP = 4;
+  for (int u0 = g; u0 < Wr; u0 += UP * ng) {
+    float bv[UP];
+    int bk[UP];
+#pragma unroll
+    for (int e = 0; e < UP; e++) {
+      const int uu = min(u0 + e * ng, W - 1);
+      lane_best(agg_tar + (row + uu) * D, D, l, vec4, bv[e], bk[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < UP; e++) {
+      const int u = u0 + e * ng;
+      const int k = group_reduce(bv[e], bk[e]);
+      if (l == 0 && u < W) {
+        kr_s[u] = (int16_t)k;
+        if (wta_tar) wta_tar[row + u] = (int16_t)k;
+      }
     }
   }
   __syncthreads();
   const float sv = (float)shift[(size_t)b * H + v];
-  for (int u = g; u < Wr; u += ng) {
-    const int uu = min(u, W - 1);
-    const float* p = agg_ref + (row + uu) * D;
-    const int k = group_argmax(p, D, l, vec4);
-    if (l != 0 || u >= W) continue;
-    if (wta_ref) wta_ref[row + u] = (int16_t)k;
-    float d = qnan();
-    if (k >= 0) {
-      const int up = u - (k + d_lo);
-      if (up >= 0 && up < W) {
-        const int kr = kr_s[up];
-        if (kr >= 0 && abs(k - kr) <= tol) {
-          float r = (float)(k + d_lo);
-          if (subpix && k >= 1 && k <= D - 2) {
-            const float a = p[k - 1], bb = p[k], c = p[k + 1];
-            const float den = 2.f * a + 2.f * c - 4.f * bb;
-            if (!(a != a) && !(c != c) && fabsf(den) > 1e-12f) r += __fdiv_rn(a - c, den);
+  for (int u0 = g; u0 < Wr; u0 += UP * ng) {
+    float bv[UP];
+    int bk[UP];
+#pragma unroll
+    for (int e = 0; e < UP; e++) {
+      const int uu = min(u0 + e * ng, W - 1);
+      lane_best(agg_ref + (row + uu) * D, D, l, vec4, bv[e], bk[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < UP; e++) {
+      const int u = u0 + e * ng;
+      const int k = group_reduce(bv[e], bk[e]);
+      if (l != 0 || u >= W) continue;
+      const float* p = agg_ref + (row + u) * D;
+      if (wta_ref) wta_ref[row + u] = (int16_t)k;
+      float d = qnan();
+      if (k >= 0) {
+        const int up = u - (k + d_lo);
+        if (up >= 0 && up < W) {
+          const int kr = kr_s[up];
+          if (kr >= 0 && abs(k - kr) <= tol) {
+            float r = (float)(k + d_lo);
+            if (subpix && k >= 1 && k <= D - 2) {
+              const float a = p[k - 1], bb = p[k], c = p[k + 1];
+              const float den = 2.f * a + 2.f * c - 4.f * bb;
+              if (!(a != a) && !(c != c) && fabsf(den) > 1e-12f) r += __fdiv_rn(a - c, den);
+            }
+            d = r + sv;
           }
-          d = r + sv;
         }
       }
+      disp[row + u] = d;
     }
-    disp[row + u] = d;
   }
 }
 

@@ -33,7 +33,8 @@ namespace rsr {
 // ---------------------------------------------------------------------------
 constexpr int ST_TX = 64, ST_TY = 16;
 
-__global__ void __launch_bounds__(256) k_block_stats(int H, int W, int p,
+template <int p>
+__global__ void __launch_bounds__(256) k_block_stats(int H, int W,
                                                      const uint8_t* __restrict__ img,
                                                      const uint8_t* __restrict__ mask,
                                                      int32_t* __restrict__ Sout,
@@ -66,47 +67,38 @@ __global__ void __launch_bounds__(256) k_block_stats(int H, int W, int p,
     }
   }
   __syncthreads();
-  // vertical sliding sums, one column per thread
-  for (int c = threadIdx.x; c < TC; c += blockDim.x) {
+  // vertical (2p+1)-sums: one (row, column) item per thread iteration, all threads busy
+  constexpr int K = 2 * p + 1;
+  for (int it = threadIdx.x; it < ST_TY * TC; it += blockDim.x) {
+    const int y = it / TC, c = it % TC;
     int s = 0, ss = 0, m = 0;
-    for (int r = 0; r < 2 * p + 1; r++) {
-      const int v = pix[r * TC + c];
-      s += v; ss += v * v; m += msk[r * TC + c];
+#pragma unroll
+    for (int r = 0; r < K; r++) {
+      const int v = pix[(y + r) * TC + c];
+      s += v; ss += v * v; m += msk[(y + r) * TC + c];
     }
-    for (int y = 0; y < ST_TY; y++) {
-      cS[y * TC + c] = s; cSS[y * TC + c] = ss; cM[y * TC + c] = m;
-      if (y + 1 < ST_TY) {
-        const int vin = pix[(y + 2 * p + 1) * TC + c], vout = pix[y * TC + c];
-        s += vin - vout; ss += vin * vin - vout * vout;
-        m += msk[(y + 2 * p + 1) * TC + c] - msk[y * TC + c];
-      }
-    }
+    cS[it] = s; cSS[it] = ss; cM[it] = m;
   }
   __syncthreads();
-  // horizontal sliding sums over chunks of 16 columns
-  const int n = (2 * p + 1) * (2 * p + 1);
-  for (int it = threadIdx.x; it < ST_TY * (ST_TX / 16); it += blockDim.x) {
-    const int y = it / (ST_TX / 16), xc = (it % (ST_TX / 16)) * 16;
+  // horizontal (2p+1)-sums: one output pixel per thread iteration (coalesced stores)
+  const int n = K * K;
+  for (int it = threadIdx.x; it < ST_TY * ST_TX; it += blockDim.x) {
+    const int y = it / ST_TX, x = it % ST_TX;
+    const int yy = y0 + y, xx = x0 + x;
+    if (yy >= H || xx >= W) continue;
     int s = 0, ss = 0, m = 0;
-    for (int d = 0; d < 2 * p + 1; d++) {
-      s += cS[y * TC + xc + d]; ss += cSS[y * TC + xc + d]; m += cM[y * TC + xc + d];
+#pragma unroll
+    for (int d = 0; d < K; d++) {
+      s += cS[y * TC + x + d]; ss += cSS[y * TC + x + d]; m += cM[y * TC + x + d];
     }
-    const int yy = y0 + y;
-    for (int i = 0; i < 16; i++) {
-      const int xx = x0 + xc + i;
-      if (yy < H && xx < W) {
-        const bool inside = yy >= p && yy <= H - 1 - p && xx >= p && xx <= W - 1 - p;
-        const long long var = (long long)n * ss - (long long)s * s;
-        const bool ok = inside && m == n && var != 0;
-        const size_t g = base + (size_t)yy * W + xx;
-        Sout[g] = s;
-        inv[g] = ok ? (float)(1.0 / sqrt((double)var)) : qnan();
-      }
-      if (i + 1 < 16) {
-        const int a = y * TC + xc + i + 2 * p + 1, o = y * TC + xc + i;
-        s += cS[a] - cS[o]; ss += cSS[a] - cSS[o]; m += cM[a] - cM[o];
-      }
-    }
+    const bool inside = yy >= p && yy <= H - 1 - p && xx >= p && xx <= W - 1 - p;
+    // exact integer variance (int64: n * sum(i^2) reaches 3.3e9 at p = 7); its fp32
+    // rounding and MUFU.RSQ stay ~1e-7 relative, far inside the ZNCC tolerance
+    const long long var = (long long)n * ss - (long long)s * s;
+    const bool ok = inside && m == n && var != 0;
+    const size_t g = base + (size_t)yy * W + xx;
+    Sout[g] = s;
+    inv[g] = ok ? rsqrtf((float)var) : qnan();
   }
 }
 
@@ -116,7 +108,13 @@ cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* im
   const int TC = ST_TX + 2 * p, TR = ST_TY + 2 * p;
   const size_t smem = sizeof(int) * (size_t)(2 * TR * TC + 3 * ST_TY * TC);
   dim3 grid((W + ST_TX - 1) / ST_TX, (H + ST_TY - 1) / ST_TY, B);
-  k_block_stats<<<grid, 256, smem, st>>>(H, W, p, img, mask, S, inv);
+  switch (p) {
+#define RSR_BS(PP) \
+  case PP: k_block_stats<PP><<<grid, 256, smem, st>>>(H, W, img, mask, S, inv); break;
+    RSR_BS(1) RSR_BS(2) RSR_BS(3) RSR_BS(4) RSR_BS(5) RSR_BS(6) RSR_BS(7)
+#undef RSR_BS
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
