@@ -17,11 +17,15 @@ cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* im
                                const uint8_t* mask, int32_t* S, float* inv, cudaStream_t st);
 
 // NCC volume in [B][H][W][D] layout. tar=false: vol[v][u][k] = c(u, v, r);
-// tar=true: vol[v][u'][k] = c(u'+r, v, r).  nan_map optional.
+// tar=true: vol[v][u'][k] = c(u'+r, v, r).
 cudaError_t launch_zncc(bool tar, int B, int H, int W, int rho_b, int d_lo, int D,
                         const uint8_t* ref, const uint8_t* warped, const int32_t* SL,
                         const float* invL, const int32_t* SW, const float* invW, float* vol,
-                        uint8_t* nan_map, cudaStream_t st);
+                        cudaStream_t st);
+
+// Per-pixel NaN summaries of both volumes, from the block norms (either map optional).
+cudaError_t launch_nan_maps(int B, int H, int W, int d_lo, int D, const float* invL,
+                            const float* invW, uint8_t* nan_ref, uint8_t* nan_tar, cudaStream_t st);
 
 cudaError_t launch_aggregate(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r,
                              const float* vol, const uint8_t* guide, const uint8_t* nan_map,

@@ -160,21 +160,18 @@ __host__ __device__ inline ZnccGeom zncc_geom(int p, int D) {
 __host__ __device__ inline size_t zncc_smem(int p, int D) {
   const ZnccGeom g = zncc_geom(p, D);
   // ring: F rows, oriented G rows x2; statistics double buffer: sF, iF, sG x2, iG x2
-  return sizeof(float) * ((size_t)g.NRING * (g.FC + 2 * g.GROW) + 2 * (2 * ZTX + 4 * (size_t)g.SROW2)) +
-         sizeof(int) * (ZTX / ZX);
+  return sizeof(float) * ((size_t)g.NRING * (g.FC + 2 * g.GROW) + 2 * (2 * ZTX + 4 * (size_t)g.SROW2));
 }
 
 template <int P, bool TAR>
 __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(int H, int W, int d_lo, int D, int Dst, int koff,
-                                              bool nan_accumulate,
                                               const uint8_t* __restrict__ ref,
                                               const uint8_t* __restrict__ warped,
                                               const int32_t* __restrict__ SLg,
                                               const float* __restrict__ invLg,
                                               const int32_t* __restrict__ SWg,
                                               const float* __restrict__ invWg,
-                                              float* __restrict__ vol,
-                                              uint8_t* __restrict__ nan_map) {
+                                              float* __restrict__ vol) {
   constexpr int NJ = ZX + 2 * P;          // V columns per thread
   constexpr int NQP = ZR / 2;             // disparity pairs per thread
   constexpr int NGR = NJ + ZR;            // oriented G run loaded per row (>= NJ + ZR - 1)
@@ -187,7 +184,6 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
   float* Gs = Fs + gm.NRING * gm.FC;                 // [NRING][GROW]  oriented G image rows
   float* Gs1 = Gs + gm.NRING * gm.GROW;              // [NRING][GROW]  shifted by one entry
   float* St = Gs1 + gm.NRING * gm.GROW;              // [2][sF ZTX | iF ZTX | sG | sG1 | iG | iG1]
-  int* flags = reinterpret_cast<int*>(St + 2 * (2 * ZTX + 4 * gm.SROW2));  // [ZTX/ZX] 4 x 2 bits
   const int SROW = 2 * ZTX + 4 * gm.SROW2;
 
   const int b = blockIdx.z, x0 = blockIdx.x * ZTX, y0 = blockIdx.y * ZBY;
@@ -284,7 +280,6 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
     fetch(t, t == 0 ? 0 : -1);
     commit(t, t == 0 ? 0 : -1);
   }
-  if (threadIdx.x < ZTX / ZX) flags[threadIdx.x] = 0;
   __syncthreads();
 
   const int n_rg = (D + ZR - 1) / ZR;
@@ -376,12 +371,7 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
       // NaN structure from the statistics alone (num is always finite): c(i, q) is NaN
       // iff iF[i] or the G-side norm of (i, q) is NaN; over q those are the oriented
       // entries [oi, oi + ZR) with oi = TAR ? i : ZX - 1 - i.
-      uint32_t gnan = 0;
-#pragma unroll
-      for (int m = 0; m < ZX + ZR - 1; m++) gnan |= (iGe[m] != iGe[m] ? 1u : 0u) << m;
       const int nq = min(ZR, d_hi - r0 + 1);   // disparities of this thread inside the slab
-      const uint32_t qmask = nq >= ZR ? 0xFFu : ((1u << max(nq, 0)) - 1u);
-      int fl4 = 0;
       float2 hs[NQP];
 #pragma unroll
       for (int qp = 0; qp < NQP; qp++) {
@@ -428,28 +418,9 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
               if (q < nq) dst[q] = (q & 1) ? out[q >> 1].y : out[q >> 1].x;
           }
         }
-        const bool fnan = iF[i] != iF[i];
-        const uint32_t win = (gnan >> oi) & qmask;   // oriented: entry oi + q <-> disparity q
-        const bool anynan = nq > 0 && (fnan || win != 0);
-        const bool anyfin = nq > 0 && !fnan && win != qmask;
-        fl4 |= ((anynan ? 1 : 0) | (anyfin ? 2 : 0)) << (8 * i);
-      }
-      if (nan_map && fl4) atomicOr(&flags[cg], fl4);
-    }
-    __syncthreads();   // ring slot of row y - 1 and St[(y + 1) & 1] are free; flags complete
-    if (nan_map && threadIdx.x < ZTX / ZX) {
-      const int fl4 = flags[threadIdx.x];
-      flags[threadIdx.x] = 0;
-      const int yy = y0 + y;
-#pragma unroll
-      for (int i = 0; i < ZX; i++) {
-        const int xx = x0 + ZX * threadIdx.x + i;
-        if (xx < W) {
-          uint8_t* mp = nan_map + ibase + (size_t)yy * W + xx;
-          *mp = (uint8_t)(((fl4 >> (8 * i)) & 3) | (nan_accumulate ? *mp : 0));
-        }
       }
     }
+    __syncthreads();   // ring slot of row y - 1 and St[(y + 1) & 1] are free
     if (more) commit(y + 1 + 2 * P, y + 1);
     __syncthreads();
   }
@@ -457,10 +428,10 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
 
 template <int P, bool TAR>
 static cudaError_t zncc_launch_t(int B, int H, int W, int d_lo, int D, int Dst, int koff,
-                                 bool nan_acc, const uint8_t* ref,
+                                 const uint8_t* ref,
                                  const uint8_t* warped, const int32_t* SL, const float* invL,
                                  const int32_t* SW, const float* invW, float* vol,
-                                 uint8_t* nan_map, cudaStream_t st) {
+                                 cudaStream_t st) {
   const size_t smem = zncc_smem(P, D);
   auto kern = k_zncc<P, TAR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -471,29 +442,100 @@ static cudaError_t zncc_launch_t(int B, int H, int W, int d_lo, int D, int Dst, 
   static_assert(2 * 128 >= 84 + 152 && 4 * 128 >= 2 * ZTX + 2 * 136, "row load lists must fit the prefetch");
   // threads > 1024 is rejected by the API (D > 512 would need a k-slab split)
   dim3 grid((W + ZTX - 1) / ZTX, (H + ZBY - 1) / ZBY, B);
-  kern<<<grid, threads, smem, st>>>(H, W, d_lo, D, Dst, koff, nan_acc, ref, warped, SL, invL, SW,
-                                    invW, vol, nan_map);
+  kern<<<grid, threads, smem, st>>>(H, W, d_lo, D, Dst, koff, ref, warped, SL, invL, SW, invW, vol);
+  return cudaGetLastError();
+}
+
+// Per-pixel NaN summaries straight from the block statistics: an NCC cost is NaN
+// exactly when the left or the right block norm is (the numerator is always
+// finite), so for the reference volume, pixel u has some finite cost iff inv_L(u)
+// is finite and some inv_W(u - r), r in [d_lo, d_hi], is, and some NaN cost iff
+// inv_L(u) is NaN or one of those is NaN or outside the image; symmetrically for the
+// target volume with inv_W(u') and inv_L(u' + r).  One CTA per (row, frame):
+// prefix counts of finite norms along the row make each pixel O(1).
+__global__ void __launch_bounds__(256) k_nan_maps(int H, int W, int d_lo, int D,
+                                                  const float* __restrict__ invL,
+                                                  const float* __restrict__ invW,
+                                                  uint8_t* __restrict__ nan_ref,
+                                                  uint8_t* __restrict__ nan_tar) {
+  extern __shared__ int nm_smem[];
+  int* cL = nm_smem;          // [W + 1] prefix counts of finite inv_L
+  int* cW = cL + (W + 1);     // [W + 1] prefix counts of finite inv_W
+  const int v = blockIdx.x, b = blockIdx.y;
+  const size_t row = ((size_t)b * H + v) * W;
+  __shared__ int wsumL[32], wsumW[32];
+  // block-wide exclusive scans, 256-column chunks
+  int carryL = 0, carryW = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c0 = 0; c0 < W; c0 += blockDim.x) {
+    const int c = c0 + threadIdx.x;
+    int fl = 0, fw = 0;
+    if (c < W) {
+      const float a = invL[row + c], w = invW[row + c];
+      fl = a == a; fw = w == w;
+    }
+    int sl = fl, sw = fw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int tl = __shfl_up_sync(0xffffffffu, sl, o), tw = __shfl_up_sync(0xffffffffu, sw, o);
+      if (lane >= o) { sl += tl; sw += tw; }
+    }
+    if (lane == 31) { wsumL[warp] = sl; wsumW[warp] = sw; }
+    __syncthreads();
+    int offL = carryL, offW = carryW;
+    for (int q = 0; q < warp; q++) { offL += wsumL[q]; offW += wsumW[q]; }
+    if (c < W) { cL[c + 1] = offL + sl; cW[c + 1] = offW + sw; }
+    for (int q = 0; q < nw; q++) { carryL += wsumL[q]; carryW += wsumW[q]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { cL[0] = 0; cW[0] = 0; }
+  __syncthreads();
+  auto count = [&](const int* cnt, int a, int bcol) {   // finite entries in columns [a, b]
+    a = max(a, 0);
+    bcol = min(bcol, W - 1);
+    return bcol < a ? 0 : cnt[bcol + 1] - cnt[a];
+  };
+  for (int u = threadIdx.x; u < W; u += blockDim.x) {
+    const bool lok = cL[u + 1] - cL[u] != 0, wok = cW[u + 1] - cW[u] != 0;
+    if (nan_ref) {
+      const int fin = lok ? count(cW, u - (d_lo + D - 1), u - d_lo) : 0;
+      nan_ref[row + u] = (uint8_t)((fin < D ? 1 : 0) | (fin > 0 ? 2 : 0));
+    }
+    if (nan_tar) {
+      const int fin = wok ? count(cL, u + d_lo, u + d_lo + D - 1) : 0;
+      nan_tar[row + u] = (uint8_t)((fin < D ? 1 : 0) | (fin > 0 ? 2 : 0));
+    }
+  }
+}
+
+cudaError_t launch_nan_maps(int B, int H, int W, int d_lo, int D, const float* invL,
+                            const float* invW, uint8_t* nan_ref, uint8_t* nan_tar, cudaStream_t st) {
+  if (!nan_ref && !nan_tar) return cudaSuccess;
+  const size_t smem = sizeof(int) * 2 * ((size_t)W + 1);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k_nan_maps, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_nan_maps<<<dim3(H, B), 256, smem, st>>>(H, W, d_lo, D, invL, invW, nan_ref, nan_tar);
   return cudaGetLastError();
 }
 
 cudaError_t launch_zncc(bool tar, int B, int H, int W, int rho_b, int d_lo, int D,
                         const uint8_t* ref, const uint8_t* warped, const int32_t* SL,
                         const float* invL, const int32_t* SW, const float* invW, float* vol,
-                        uint8_t* nan_map, cudaStream_t st) {
-  // Disparity slabs of at most 64 (<= 128 threads per CTA); later slabs OR
-  // their NaN flags into the map written by the first.
+                        cudaStream_t st) {
+  // Disparity slabs of at most 64 (<= 128 threads per CTA).
   constexpr int SLAB = 64;
   for (int k0 = 0; k0 < D; k0 += SLAB) {
     const int Ds = D - k0 < SLAB ? D - k0 : SLAB;
     const int dl = d_lo + k0;
-    const bool acc = k0 > 0;
     cudaError_t e;
 #define RSR_Z(PP)                                                                                \
   case PP:                                                                                       \
-    e = tar ? zncc_launch_t<PP, true>(B, H, W, dl, Ds, D, k0, acc, ref, warped, SL, invL, SW,     \
-                                      invW, vol, nan_map, st)                                    \
-            : zncc_launch_t<PP, false>(B, H, W, dl, Ds, D, k0, acc, ref, warped, SL, invL, SW,    \
-                                       invW, vol, nan_map, st);                                  \
+    e = tar ? zncc_launch_t<PP, true>(B, H, W, dl, Ds, D, k0, ref, warped, SL, invL, SW, invW,    \
+                                      vol, st)                                                   \
+            : zncc_launch_t<PP, false>(B, H, W, dl, Ds, D, k0, ref, warped, SL, invL, SW, invW,   \
+                                       vol, st);                                                 \
     break;
     switch (rho_b) {
       RSR_Z(1) RSR_Z(2) RSR_Z(3) RSR_Z(4) RSR_Z(5) RSR_Z(6) RSR_Z(7)
