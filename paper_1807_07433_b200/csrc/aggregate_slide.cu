@@ -21,21 +21,21 @@
 //    row inside the last tap's FFMA2s (destination = next-younger register),
 //    so the loop needs no unrolling over ages and no register moves.
 //  * Warp roles (mbarrier hand-off, no CTA barrier inside a segment): G
-//    consumer warps (FFMA2, fma.rn.f32x2 with a scalar weight operand),
-//    3 weight-producer warps (exp2 on the MUFU pipe, once per (pixel, tap) per
-//    CTA, per-pixel weight sums), 1 stager warp (cost rows by cp.async.bulk,
-//    the TMA engine, 4-stage ring).
-//  * Persistent CTAs: one CTA per SM walks an equal share of the linearised
-//    (frame, slab, strip, row) space in segments of <= 720 rows, so the grid
-//    has no wave-quantisation tail and a strip pays its 2 rho warm-up rows once
-//    per segment.
+//    consumer warps (FFMA2, fma.rn.f32x2 with a scalar weight operand) and 4
+//    producer warps.  Producers compute each weight once per (pixel, tap) per
+//    CTA as w = S(dx, dy) * R(g(q) - g(p)): the spatial factor exp2(kd (dx^2 +
+//    dy^2)) lives in registers for the whole kernel, the range factor
+//    exp2(kr dg^2) comes from a shared table indexed by the integer guide
+//    difference (skipped pixels index its zero tail).  Producer warp 0 also
+//    stages the cost rows (cp.async.bulk, the TMA engine, 4-stage ring).
+//  * One CTA per (32-column strip, chunk of R rows, frame x slab); strips are
+//    launched edge-first (longest-first scheduling of the general path).
 //  * Tiles whose footprint holds no partially-NaN pixel (nan_map) take the
 //    "clean" path: NaN-free costs (all-NaN or outside pixels get weight 0 and
 //    cost 0) and one denominator per pixel.  Other segments take the exact
 //    general path: pairs (C0, V) = (cost or 0, validity) so the same FFMA2
 //    accumulates numerator and per-disparity denominator, two passes per slab.
-#include <cuda_fp16.h>
-
+//    Both accumulate in the same order, so they agree bitwise where both apply.
 #include <cmath>
 
 #include "common.cuh"
@@ -47,10 +47,12 @@ constexpr int SG_NPROD = 4;     // weight-producer warps (warp 0 also stages cos
 constexpr int SG_NSC = 4;       // cost stages
 constexpr int SG_NSW = 3;       // weight stages
 constexpr int SG_SEGMAX = 720;  // max output rows per segment (guide tile height)
+constexpr short SG_GSKIP = 600;     // integer guide tile: skipped pixel (outside / all-NaN)
+constexpr int SG_RLUT = 2 * 600 + 255 + 1;   // range table, zero beyond |dg| = 255
 
 struct SlideGeom {
   int G, KS, nslab, CX, XS, WST, GR;
-  size_t off_cost, off_w, off_dpart, off_guide, off_tapf, off_bar, bytes;
+  size_t off_cost, off_w, off_dpart, off_guide, off_rlut, off_bar, bytes;
 };
 
 // KS = disparities per slab (multiple of 8, <= 64), G = consumer lanes per column
@@ -69,9 +71,9 @@ __host__ __device__ inline SlideGeom slide_geom(int D, int rho) {
   g.off_cost = o;  o += sizeof(float) * (size_t)SG_NSC * g.CX * g.KS;
   g.off_w = o;     o += sizeof(float) * (size_t)SG_NSW * g.WST;
   g.off_dpart = o; o += sizeof(float) * (size_t)NT * 32;
-  g.off_guide = o; o += sizeof(__half) * (size_t)g.GR * g.CX;
+  g.off_guide = o; o += sizeof(short) * (size_t)g.GR * g.CX;
   o = (o + 15) & ~size_t(15);
-  g.off_tapf = o;  o += sizeof(float) * 2 * (size_t)g.CX;
+  g.off_rlut = o;  o += sizeof(float) * (size_t)SG_RLUT;
   o = (o + 15) & ~size_t(15);
   g.off_bar = o;   o += 8 * (2 * SG_NSC + 2 * SG_NSW);
   g.bytes = o;
@@ -141,7 +143,7 @@ RSR_DEVINL Seg cta_segment(const SlideArgs& A, const SlideGeom& g) {
 // or NaN (general path).
 template <int RHO>
 __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g, const Seg& s, bool clean,
-                                          int i, const __half* gt, float* cost_s, uint64_t* full_c, uint64_t* empty_c,
+                                          int i, const short* gt, float* cost_s, uint64_t* full_c, uint64_t* empty_c,
                                           uint32_t& it_c, int lane) {
   const bool bulk = (A.D & 3) == 0;
   const float fillv = clean ? 0.f : qnan();
@@ -159,7 +161,8 @@ __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g
     const int xx = s.x0 - RHO + col;
     // the guide tile marks outside and all-NaN pixels (+inf): fill them instead of copying
     // (all-NaN -> 0 on a clean segment, where such taps carry weight 0; NaN otherwise)
-    const bool skip = !(col < g.CX && row_in) || __hisinf(gt[(i + RHO) * g.CX + col]) != 0;
+    const bool skip = !(col < g.CX && row_in) ||
+                      gt[(i + RHO) * g.CX + col] == SG_GSKIP;
     cp[h] = !skip && bulk;
     if (col < g.CX) {
       float* d = dst + col * g.KS;
@@ -207,80 +210,69 @@ __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g
 // independence).  Warp 0 also stages the cost rows.
 template <int RHO>
 __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideGeom& g, const Seg& s,
-                                                bool clean, int npass, const __half* gt, float* w_s,
-                                                float* dsum, float* tapf, float* cost_s, uint64_t* full_w,
+                                                bool clean, int npass, const short* gt, float* w_s,
+                                                float* dsum, float* cost_s, uint64_t* full_w,
                                                 uint64_t* empty_w, uint64_t* full_c, uint64_t* empty_c,
-                                                uint32_t& it_w, uint32_t& it_c, int p, int lane) {
+                                                uint32_t& it_w, uint32_t& it_c, int p, int lane,
+                                                const float* rlut) {
   constexpr int NT = 2 * RHO + 1;
   constexpr int NAB = (NT + 3) / 4;          // age blocks of 4
   const int NR = (s.yb - s.ya) + 2 * RHO;
   const int xs = lane >> 2, as = lane & 3;
+  float sreg[NAB][NT];   // exp2(kd (dx^2 + dy^2)) for this lane's ages
+#pragma unroll
+  for (int n = 0; n < NAB; n++) {
+    const int a = min(((p + 4 * n) % NAB) * 4 + as, NT - 1);
+#pragma unroll
+    for (int j = 0; j < NT; j++)
+      sreg[n][j] = ex2_ftz((float)((j - RHO) * (j - RHO) + (RHO - a) * (RHO - a)) * A.kd);
+  }
   for (int pass = 0; pass < npass; pass++) {
     for (int e = p * 32 + lane; e < NT * 32; e += SG_NPROD * 32) dsum[e] = 0.f;
-    // tap row 0 as float (the tile is fp16; converting once per row instead of once per weight)
-    for (int c = p * 32 + lane; c < g.CX; c += SG_NPROD * 32) tapf[c] = __half2float(gt[RHO * g.CX + c]);
     asm volatile("bar.sync 1, %0;" ::"r"(SG_NPROD * 32) : "memory");
     for (int i = 0; i < NR; i++, it_w++) {
       if (p == 0) stage_row<RHO>(A, g, s, clean, i, gt, cost_s, full_c, empty_c, it_c, lane);
       const int st = it_w % SG_NSW;
       if (it_w >= SG_NSW) mbar_wait_parity(&empty_w[st], ((it_w / SG_NSW) & 1) ^ 1);
       float* wst = w_s + (size_t)st * g.WST;
-      const float* trow = tapf + (i & 1) * g.CX;   // tap row r (tile row i + RHO) as float
       // this warp's items (x-block, age-block) = p + 4 n, n < NAB; all shared-memory
       // loads first, then the math, then the stores: the tile, the running sums and
       // the weight stage may alias as far as the compiler knows, so interleaving them
       // would serialise every tap's LDS -> MUFU -> STS chain
       static_assert(SG_NPROD == 4, "items are dealt to 4 producer warps");
-      float wv[NAB][NT], gp[NAB], den[NAB];
-#pragma unroll
-      for (int n = 0; n < NAB; n++) {
-        const int item = p + 4 * n;
-        const int x = (item / NAB) * 8 + xs, a = min((item % NAB) * 4 + as, NT - 1);
-        // centre of age a: output row r - RHO + a = guide tile row i + a, column x + RHO.
-        // Skipped pixels (outside / all-NaN) are +inf in the tile and -inf as a centre,
-        // so dg = +-inf and every weight touching them is exp2(-inf) = 0 exactly
-        // (kr < 0 also for gamma_r = inf, where kr = -1e-30).
-        const float cg = __half2float(gt[(i + a) * g.CX + x + RHO]);
-        gp[n] = isinf(cg) ? -cg : cg;
-        den[n] = dsum[((i + a) % NT) * 32 + x];
-#pragma unroll
-        for (int j = 0; j < NT; j++) wv[n][j] = (float)trow[x + j];
-      }
-#pragma unroll
-      for (int n = 0; n < NAB; n++) {
-        const int a = min(((p + 4 * n) % NAB) * 4 + as, NT - 1);
-        const float cy = (float)((RHO - a) * (RHO - a)) * A.kd;
-#pragma unroll
-        for (int j = 0; j < NT; j++) {
-          const float dg = wv[n][j] - gp[n];
-          wv[n][j] = ex2_ftz(fmaf(dg * A.kr, dg, (float)((j - RHO) * (j - RHO)) * A.kd + cy));
-        }
-      }
+      // w = S(a, j) * R(g(q) - g(p)): spatial factor per (age, tap) held in registers
+      // for the whole kernel (sreg), range factor from a shared table indexed by the
+      // integer guide difference (skipped pixels index the zero tail of the table).
+      const short* trs = gt + (i + RHO) * g.CX;   // tap row r
 #pragma unroll
       for (int n = 0; n < NAB; n++) {
         const int item = p + 4 * n;
         const int x = (item / NAB) * 8 + xs, a = (item % NAB) * 4 + as;
+        const int ac = min(a, NT - 1);
+        int gp = gt[(i + ac) * g.CX + x + RHO];
+        gp = (gp == SG_GSKIP) ? -SG_GSKIP : gp;
+        float* slot = dsum + ((i + ac) % NT) * 32 + x;
+        float d = *slot;
+        float w[NT];
+#pragma unroll
+        for (int j = 0; j < NT; j++) w[j] = sreg[n][j] * rlut[trs[x + j] - gp + 255];
         if (a < NT) {
           float* wd = wst + x * g.XS + a;
-          float d = den[n];
 #pragma unroll
           for (int j = 0; j < NT; j++) {
-            wd[j * 16] = wv[n][j];
-            d += wv[n][j];
+            wd[j * 16] = w[j];
+            d += w[j];
           }
           if (a == 0) {   // the output row completing at input row i
             wst[32 * g.XS + x] = d;
-            dsum[((i + a) % NT) * 32 + x] = 0.f;
+            *slot = 0.f;
           } else {
-            dsum[((i + a) % NT) * 32 + x] = d;
+            *slot = d;
           }
         }
       }
       // next tap row as float into the other buffer (its last readers finished before
       // the previous barrier)
-      if (i + 1 < NR)
-        for (int c = p * 32 + lane; c < g.CX; c += SG_NPROD * 32)
-          tapf[((i + 1) & 1) * g.CX + c] = __half2float(gt[(i + 1 + RHO) * g.CX + c]);
       asm volatile("bar.sync 1, %0;" ::"r"(SG_NPROD * 32) : "memory");   // row sums handed to the next age
       mbar_arrive(&full_w[st]);
     }
@@ -407,8 +399,13 @@ __global__ void __launch_bounds__(384, 1) k_aggregate_slide(const SlideArgs A) {
   float* cost_s = reinterpret_cast<float*>(sl_smem + g.off_cost);
   float* w_s = reinterpret_cast<float*>(sl_smem + g.off_w);
   float* dpart = reinterpret_cast<float*>(sl_smem + g.off_dpart);
-  __half* gt = reinterpret_cast<__half*>(sl_smem + g.off_guide);
-  float* tapf = reinterpret_cast<float*>(sl_smem + g.off_tapf);
+  short* gt = reinterpret_cast<short*>(sl_smem + g.off_guide);
+  float* rlut = reinterpret_cast<float*>(sl_smem + g.off_rlut);
+  // range factor exp2(kr dg^2) at index dg + 255; zero for the skip encodings
+  for (int t = threadIdx.x; t < SG_RLUT; t += blockDim.x) {
+    const int dg = t - 255;
+    rlut[t] = (dg >= -255 && dg <= 255) ? ex2_ftz((float)(dg * dg) * A.kr) : 0.f;
+  }
   uint64_t* full_c = reinterpret_cast<uint64_t*>(sl_smem + g.off_bar);
   uint64_t* empty_c = full_c + SG_NSC;
   uint64_t* full_w = empty_c + SG_NSC;
@@ -457,15 +454,15 @@ __global__ void __launch_bounds__(384, 1) k_aggregate_slide(const SlideArgs A) {
           const int yy = s.ya - 2 * RHO + e / g.CX;
           if (mv[u] == 3 && yy >= s.ya - RHO && yy < s.yb + RHO) partial = 1;
           // +inf marks a skipped pixel (outside the image or all-NaN)
-          gt[e] = mv[u] == 1 ? __ushort_as_half(0x7C00) : __ushort2half_rn(gv[u]);
+          gt[e] = mv[u] == 1 ? SG_GSKIP : (short)gv[u];
         }
       }
     }
     const bool clean = !__syncthreads_or(partial);
     const int npass = clean ? 1 : 2;
     if (warp >= n_cons) {
-      produce_weights<RHO>(A, g, s, clean, npass, gt, w_s, dpart, tapf, cost_s, full_w, empty_w, full_c, empty_c,
-                           it, it_c, warp - n_cons, lane);
+      produce_weights<RHO>(A, g, s, clean, npass, gt, w_s, dpart, cost_s, full_w, empty_w, full_c, empty_c,
+                           it, it_c, warp - n_cons, lane, rlut);
     } else {
       const int t = tid;   // consumer thread: column t / G, lane-in-group t % G
       if (clean)

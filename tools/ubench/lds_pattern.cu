@@ -48,6 +48,8 @@ __device__ __forceinline__ void load_tap(const float* cb, const float* wb, int j
   }
 }
 
+// mode 6: no shared-memory loads; every tap refreshes all 21 operand registers with
+// an ALU op (LOP3 bit flip of the lowest mantissa bit): "fresh operands" without LDS
 template <int MODE>
 __global__ void k(float* out, int iters) {
   __shared__ __align__(16) float sm[4096];
@@ -62,7 +64,24 @@ __global__ void k(float* out, int iters) {
   const float* cb = sm + (lane & 7) * 4;
   const float* wb = sm + 1024 + (lane >> 3) * 20;
   for (int it = 0; it < iters; it++) {
-    if (MODE == 3 || MODE == 5) {
+    if (MODE == 6) {
+      float wv[16]; float2 cp[4];
+#pragma unroll
+      for (int a = 0; a < 16; a++) wv[a] = 1e-3f * (a + lane);
+#pragma unroll
+      for (int q = 0; q < 4; q++) cp[q] = make_float2(1e-3f * q, 2e-3f * lane);
+#pragma unroll
+      for (int j = 0; j < 13; j++) {
+#pragma unroll
+        for (int a = 0; a < 13; a++) wv[a] = __int_as_float(__float_as_int(wv[a]) ^ (j & 1));
+#pragma unroll
+        for (int q = 0; q < 4; q++) cp[q] = make_float2(__int_as_float(__float_as_int(cp[q].x) ^ 1), __int_as_float(__float_as_int(cp[q].y) ^ 1));
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+#pragma unroll
+          for (int a = 0; a < 13; a++) acc[a][q] = fma2s(wv[a], cp[q], acc[a][q]);
+      }
+    } else if (MODE == 3 || MODE == 5) {
       float wv[2][16]; float2 cp[2][4];
       load_tap<0>(cb, wb, 0, it, wv[0], cp[0]);
 #pragma unroll
@@ -150,7 +169,7 @@ int main() {
     printf("{\"mode\": \"kl4\", \"warps_per_smsp\": %d, \"ms\": %.3f, \"frac_of_74.45\": %.3f, \"err\": \"%s\"}\n", wps, best,
            flop / best / 1e9 / 74.45, cudaGetErrorString(cudaGetLastError()));
   }
-  for (int mode = 0; mode < 1; mode++)
+  for (int mode = 0; mode < 7; mode += 6)
     for (int wps = 1; wps <= 2; wps++) {
       int threads = 128 * wps, iters = 2000;
       auto launch = [&] {
@@ -160,6 +179,7 @@ int main() {
           case 2: k<2><<<sms, threads>>>(out, iters); break;
           case 3: k<3><<<sms, threads>>>(out, iters); break;
           case 4: k<4><<<sms, threads>>>(out, iters); break;
+          case 6: k<6><<<sms, threads>>>(out, iters); break;
           default: k<5><<<sms, threads>>>(out, iters); break;
         }
       };
