@@ -73,6 +73,19 @@ def oracle_sample(cfg, rows, frame_index=0):
     return dt, rows / cfg.height
 
 
+def k3_traffic():
+    """DRAM bytes (read + write) per K3 launch from the committed ncu --set full capture
+    of this workload (profiles/k3_traffic.json); None if absent.  Compare with
+    algorithmic_bytes_per_launch (volume read + write once)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k3_traffic.json")) as f:
+            t = json.load(f)
+        return {"bytes_per_launch": t["traffic_bytes_per_launch"],
+                "algorithmic_bytes_per_launch": t["algorithmic_bytes_per_launch"], "source": t["source"]}
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -312,7 +325,7 @@ def main():
                                               ("" if world == 1 or args.no_gather else " + NCCL gather")}),
         "roofline": {"kernel": "k_aggregate (rsr_aggregate, Eq. 8)", "bound": "alu", "achieved": achieved,
                      "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
-                     "traffic": None,
+                     "traffic": k3_traffic(),
                      "peak_note": "FP32 FMA: 148 SMs x 128 lanes x 2 flop x 1965 MHz (B200_PROFILING.md unit "
                                   "counts and max clock); measured FFMA-chain peak 71.5 TFLOP/s "
                                   "(profiles/r01_ubench_fp32_lds.jsonl)",
