@@ -284,12 +284,43 @@ template <int RHO, bool CLEAN>
 __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, const Seg& s,
                                         const float* cost_s, const float* w_s, uint64_t* full_c,
                                         uint64_t* empty_c, uint64_t* full_w, uint64_t* empty_w,
-                                        uint32_t& it, int xl, int l, int lane) {
+                                        uint32_t& it, int xl, int l, int lane, const short* gt) {
   constexpr int NT = 2 * RHO + 1;
   constexpr int NPASS = CLEAN ? 1 : 2;
   const int NR = (s.yb - s.ya) + 2 * RHO;
   const int x = s.x0 + xl;
   const bool vec_out = (A.D & 3) == 0;
+  // A warp whose output pixels are all skipped (centre outside the image or all-NaN)
+  // writes NaN and only keeps the pipeline hand-off going: no FFMA2.
+  bool live = false;
+  for (int y = s.ya + l; y < s.yb; y += g.G) live |= gt[(y - s.ya + 2 * RHO) * g.CX + xl + RHO] != SG_GSKIP;
+  if (!__any_sync(0xffffffffu, live)) {
+    for (int pass = 0; pass < NPASS; pass++) {
+      const int koff = CLEAN ? 4 * l : 4 * g.G * pass + 4 * l;
+      for (int i = 0; i < NR; i++, it++) {
+        const int stc = it % SG_NSC, stw = it % SG_NSW;
+        mbar_wait_parity(&full_c[stc], (it / SG_NSC) & 1);
+        mbar_wait_parity(&full_w[stw], (it / SG_NSW) & 1);
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&empty_c[stc]);
+          mbar_arrive(&empty_w[stw]);
+        }
+        const int y = s.ya - 2 * RHO + i;
+        if (y >= s.ya && x < A.W) {
+          float* o = A.out + (s.pix0 + (size_t)y * A.W + x) * A.D + s.k0 + koff;
+#pragma unroll
+          for (int hh = 0; hh < (CLEAN ? 2 : 1); hh++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+              const int k = s.k0 + koff + 4 * g.G * hh + q;
+              if (k < s.k0 + s.ks_eff) o[4 * g.G * hh + q] = qnan();
+            }
+        }
+      }
+    }
+    return;
+  }
   for (int pass = 0; pass < NPASS; pass++) {
     float2 acc[NT][4];
 #pragma unroll
@@ -466,9 +497,9 @@ __global__ void __launch_bounds__(384, 1) k_aggregate_slide(const SlideArgs A) {
     } else {
       const int t = tid;   // consumer thread: column t / G, lane-in-group t % G
       if (clean)
-        consume<RHO, true>(A, g, s, cost_s, w_s, full_c, empty_c, full_w, empty_w, it, t / g.G, t % g.G, lane);
+        consume<RHO, true>(A, g, s, cost_s, w_s, full_c, empty_c, full_w, empty_w, it, t / g.G, t % g.G, lane, gt);
       else
-        consume<RHO, false>(A, g, s, cost_s, w_s, full_c, empty_c, full_w, empty_w, it, t / g.G, t % g.G, lane);
+        consume<RHO, false>(A, g, s, cost_s, w_s, full_c, empty_c, full_w, empty_w, it, t / g.G, t % g.G, lane, gt);
     }
   }
 }
