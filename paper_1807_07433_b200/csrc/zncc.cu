@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
   // exact integer -> float for 0 <= v < 2^23 without the XU pipe
   auto u2f = [](uint32_t v) { return __uint_as_float(0x4B000000u | v) - 8388608.0f; };
   auto commit = [&](int t_img, int y_st) {
-    const int slot = t_img % gm.NRING;
+    const int slot = t_img % (2 * P + 2);
     if (t_img >= 0) {
 #pragma unroll
       for (int u = 0; u < NPI; u++) {
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
     for (int qp = 0; qp < NQP; qp++) V2[j][qp] = make_float2(0.f, 0.f);
 
   auto accumulate_row = [&](int t, bool subtract) {
-    const int slot = t % gm.NRING;
+    const int slot = t % (2 * P + 2);
     float f[NF4 * 4], ge[NG4 * 4], go[NG4 * 4];
     const float4* fr = reinterpret_cast<const float4*>(Fs + slot * gm.FC + f_start);
     const float4* gr = reinterpret_cast<const float4*>(Gs + slot * gm.GROW + grun);
