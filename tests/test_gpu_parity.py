@@ -182,6 +182,33 @@ def test_parity_config5_frames_batched(rsr):
         compare(gpu, ora, rows, cfg, b=b, label=f"c5[{i}]")
 
 
+def test_parity_bench_launch_configuration(rsr):
+    """The exact launch bench.py times: StereoPipeline over an 8-frame c5 batch (the
+    batch size picks K3's row chunking and grid); sampled row bands of three frames
+    against the oracle, and a bitwise rerun."""
+    cfg = synth.get_config("c5")
+    B = 8
+    left, right, ab = synth.make_batch(cfg, list(range(B)))
+    L = torch.from_numpy(left).cuda()
+    R = torch.from_numpy(right).cuda()
+    AB = torch.from_numpy(ab).cuda()
+    pipe = rsr.StereoPipeline(B, cfg.height, cfg.width, rsr.StereoParams.from_config(cfg))
+    pipe.run(L, R, AB, with_wta=True)
+    torch.cuda.synchronize()
+    g = lambda t: t.cpu().numpy()  # noqa: E731
+    gpu = dict(warped=g(pipe.warped), mask=g(pipe.valid), shift=g(pipe.shift), cost_ref=g(pipe.vol_ref),
+               cost_tar=g(pipe.vol_tar), agg_ref=g(pipe.agg_ref), agg_tar=g(pipe.agg_tar),
+               disparity=g(pipe.disparity), k_ref=g(pipe.wta_ref), k_tar=g(pipe.wta_tar), xyz=g(pipe.xyz))
+    for b, rows in ((0, (0, 6)), (3, (141, 147)), (7, (714, 720))):   # chunk edges of R = 144
+        check_warp(gpu, right[b], ab[b], b)
+        ora = O.run_pipeline(left[b], right[b], ab[b][0], ab[b][1], cfg, rows=rows)
+        compare(gpu, ora, rows, cfg, b=b, label=f"bench c5[{b}]{rows}")
+    d0 = pipe.disparity.clone()
+    pipe.run(L, R, AB, with_wta=True)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.nan_to_num(d0, nan=-7.0), torch.nan_to_num(pipe.disparity, nan=-7.0))
+
+
 EDGE_CASES = {
     # name: (H, W, d_lo, d_hi, rho_block, rho_agg, gamma_d, gamma_r, alpha, beta)
     "ragged_D7": (37, 101, -3, 3, 2, 3, 2.0, 10.0, 0.1, 2.0),
