@@ -102,3 +102,32 @@ def fit_road_model(v, d, n_hyp: int, tol: float, seed: int):
         return np.nan, np.nan, int(m.sum()), best_h
     al, be = least_squares_line(v[m], d[m])
     return al, be, int(m.sum()), best_h
+
+
+def roll_plane_fit(disparity: np.ndarray, u0: int, u1: int, v0: int, v1: int):
+    """Roll angle of the rig: least-squares plane d(u, v) = g0 + g1 u + g2 v
+    over the finite disparities of the near-field patch [v0, v1) x [u0, u1), and
+    gamma = arctan(-g1 / g2).  Normal equations in fp64, solved by Cramer's rule
+    (the plain definition of the 3x3 solve).  Returns (g0, g1, g2, gamma, n);
+    NaNs if fewer than 3 samples or a singular system."""
+    vv, uu = np.mgrid[v0:v1, u0:u1]
+    d = disparity[v0:v1, u0:u1].astype(np.float64)
+    ok = np.isfinite(d)
+    u, v, d = uu[ok].astype(np.float64), vv[ok].astype(np.float64), d[ok]
+    n = len(d)
+    if n < 3:
+        return np.nan, np.nan, np.nan, np.nan, n
+    M = np.array([[n, u.sum(), v.sum()],
+                  [u.sum(), (u * u).sum(), (u * v).sum()],
+                  [v.sum(), (u * v).sum(), (v * v).sum()]])
+    r = np.array([d.sum(), (u * d).sum(), (v * d).sum()])
+    det = np.linalg.det(M)
+    if det == 0 or not np.isfinite(det):
+        return np.nan, np.nan, np.nan, np.nan, n
+    g = []
+    for c in range(3):
+        Mc = M.copy()
+        Mc[:, c] = r
+        g.append(np.linalg.det(Mc) / det)
+    g0, g1, g2 = g
+    return g0, g1, g2, float(np.arctan(-g1 / g2)), n

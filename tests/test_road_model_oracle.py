@@ -70,3 +70,26 @@ def test_synthetic_road_plane_recovered_from_ground_truth():
     a, b, n, _ = RM.fit_road_model(v, d, 256, 1e-6, 1)
     assert abs(a - f.alpha) < 1e-8 and abs(b - f.beta) < 1e-6
     assert n > 0.5 * len(v)
+
+
+def test_roll_plane_fit_closed_form():
+    # plane d = g0 + g1 u + g2 v with a known roll: the fit recovers it exactly and
+    # gamma = arctan(-g1 / g2); equals numpy lstsq on the same samples
+    h, w = 60, 90
+    vv, uu = np.mgrid[0:h, 0:w]
+    g0, g1, g2 = 12.0, -0.004, 0.11
+    d = (g0 + g1 * uu + g2 * vv).astype(np.float64)
+    d[::7, ::5] = np.nan
+    G0, G1, G2, gam, n = RM.roll_plane_fit(d, 10, 80, 20, 60)
+    assert abs(G1 - g1) < 1e-12 and abs(G2 - g2) < 1e-12 and abs(G0 - g0) < 1e-9
+    assert abs(gam - np.arctan(-g1 / g2)) < 1e-12
+    ok = np.isfinite(d[20:60, 10:80])
+    A = np.stack([np.ones(ok.sum()), uu[20:60, 10:80][ok], vv[20:60, 10:80][ok]], 1)
+    rng = np.random.default_rng(0)
+    noisy = d[20:60, 10:80][ok] + rng.normal(0, 0.1, ok.sum())
+    dn = d.copy()
+    dn[20:60, 10:80][ok] = noisy
+    ref = np.linalg.lstsq(A, noisy, rcond=None)[0]
+    N0, N1, N2, _, _ = RM.roll_plane_fit(dn, 10, 80, 20, 60)
+    assert np.allclose([N0, N1, N2], ref, rtol=1e-9, atol=1e-12)
+    assert np.isnan(RM.roll_plane_fit(np.full((5, 5), np.nan), 0, 5, 0, 5)[0])
