@@ -177,6 +177,47 @@ typedef struct {
 int rsr_reconstruct(rsr_shape s, rsr_rig rig, const float* disparity,
                     float* xyz, void* stream);
 
+/* ------------------------------------------------------------------------ */
+/* Road model (before the path: Eq. (2)).  Robust least-squares fit */
+/* of the road's v-disparity line d = alpha * v + beta ("estimated by solving */
+/* a least squares problem with a collection of reliable correspondence      */
+/* pairs", RANSAC-LSF), e.g. from the previous frame's disparity map, giving  */
+/* the next frame's rsr_warp parameters.  Samples: the finite entries of     */
+/* disparity[b][::step_v][::step_u] in row-major order, as (v, d).  RANSAC:  */
+/* hypothesis h draws sample indices i = z(2h) mod n, j = z(2h+1) mod n       */
+/* (j = (j+1) mod n if equal), z(c) = splitmix64((seed << 32) + c); line      */
+/* a = (d_j - d_i)/(v_j - v_i), b = d_i - a v_i (v_i == v_j: no support);     */
+/* consensus |d_k - (a v_k + b)| <= inlier_tol, all in fp64 with one rounding */
+/* per operation; most inliers wins, ties to the lowest h; least squares     */
+/* (normal equations, fp64) over that consensus set.                          */
+/*   disparity : float [B][H][W] (NaN = no sample)                            */
+/*   model     : double [B][3] out {alpha (px/row), beta (px), inliers};      */
+/*               alpha = beta = NaN if fewer than 2 inliers or no hypothesis  */
+/*   workspace : device scratch of rsr_road_workspace_size() bytes, 16-byte   */
+/*               aligned, caller-owned                                        */
+/* Errors: RSR_E_ARG on NULL pointers, steps < 1, n_hyp < 1 or > 2^24,        */
+/* inlier_tol <= 0 / NaN / inf, workspace too small or misaligned.            */
+typedef struct {
+  int32_t step_u, step_v;  /* sampling grid steps (>= 1)                       */
+  int32_t n_hyp;           /* RANSAC hypotheses                                */
+  float inlier_tol;        /* consensus threshold, px                          */
+  uint32_t seed;           /* generator seed                                   */
+} rsr_road_params;
+
+size_t rsr_road_workspace_size(rsr_shape s, rsr_road_params p);
+
+int rsr_road_model(rsr_shape s, rsr_road_params p, const float* disparity, double* model,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* Roll angle of the rig: least-squares plane d(u,v) = g0 + g1 u + g2 v */
+/* over the finite disparities of the near-field patch [v0, v1) x [u0, u1)   */
+/* of each map (fp64 normal equations, Cramer's rule), gamma = atan(-g1/g2).  */
+/*   out : double [B][5] {g0, g1, g2, gamma (rad), n}; NaN if n < 3 or the    */
+/*         system is singular.                                                */
+/* Errors: RSR_E_ARG on NULL pointers or an empty / out-of-image patch.       */
+int rsr_road_roll(rsr_shape s, int32_t u0, int32_t u1, int32_t v0, int32_t v1,
+                  const float* disparity, double* out, void* stream);
+
 /* Human-readable text for a status code (static storage). */
 const char* rsr_strerror(int status);
 

@@ -36,6 +36,11 @@ class RsrRig(ctypes.Structure):
                 ("v0", ctypes.c_double), ("d_min", ctypes.c_double)]
 
 
+class RsrRoadParams(ctypes.Structure):
+    _fields_ = [("step_u", ctypes.c_int32), ("step_v", ctypes.c_int32), ("n_hyp", ctypes.c_int32),
+                ("inlier_tol", ctypes.c_float), ("seed", ctypes.c_uint32)]
+
+
 class RsrError(RuntimeError):
     def __init__(self, fn, status):
         self.status = status
@@ -60,6 +65,13 @@ def lib() -> ctypes.CDLL:
         L.rsr_aggregate.argtypes = [RsrShape, ctypes.c_int32, RsrAggParams, P, P, P, P, P]
         L.rsr_disparity.argtypes = [RsrShape, RsrDispParams, P, P, P, P, P, P, P]
         L.rsr_reconstruct.argtypes = [RsrShape, RsrRig, P, P, P]
+        L.rsr_road_workspace_size.argtypes = [RsrShape, RsrRoadParams]
+        L.rsr_road_workspace_size.restype = ctypes.c_size_t
+        L.rsr_road_model.argtypes = [RsrShape, RsrRoadParams, P, P, P, ctypes.c_size_t, P]
+        L.rsr_road_model.restype = ctypes.c_int
+        L.rsr_road_roll.argtypes = [RsrShape, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                    P, P, P]
+        L.rsr_road_roll.restype = ctypes.c_int
         L.rsr_strerror.argtypes = [ctypes.c_int]
         L.rsr_strerror.restype = ctypes.c_char_p
         L.rsr_version.restype = ctypes.c_int

@@ -105,6 +105,33 @@ int rsr_disparity(rsr_shape s, rsr_disp_params p, const float* agg_ref, const fl
                                         wta_ref, wta_tar, as_stream(stream)));
 }
 
+size_t rsr_road_workspace_size(rsr_shape s, rsr_road_params p) {
+  if (!shape_ok(s) || p.step_u < 1 || p.step_v < 1 || p.n_hyp < 1) return 0;
+  return rsr::road_workspace_size(s.batch, s.height, s.width, p.step_u, p.step_v, p.n_hyp);
+}
+
+int rsr_road_model(rsr_shape s, rsr_road_params p, const float* disparity, double* model,
+                   void* workspace, size_t workspace_bytes, void* stream) {
+  if (!shape_ok(s) || !disparity || !model || !workspace) return RSR_E_ARG;
+  if (p.step_u < 1 || p.step_v < 1 || p.n_hyp < 1 || p.n_hyp > (1 << 24)) return RSR_E_ARG;
+  if (!(p.inlier_tol > 0.f) || std::isinf(p.inlier_tol)) return RSR_E_ARG;
+  if (s.batch > 65535 || (p.n_hyp + 7) / 8 > 65535) return RSR_E_ARG;
+  if (workspace_bytes < rsr_road_workspace_size(s, p)) return RSR_E_ARG;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return RSR_E_ARG;
+  return launched(rsr::launch_road_model(s.batch, s.height, s.width, p.step_u, p.step_v, p.n_hyp,
+                                         p.inlier_tol, p.seed, disparity, model, workspace,
+                                         as_stream(stream)));
+}
+
+int rsr_road_roll(rsr_shape s, int32_t u0, int32_t u1, int32_t v0, int32_t v1, const float* disparity,
+                  double* out, void* stream) {
+  if (!shape_ok(s) || !disparity || !out) return RSR_E_ARG;
+  if (u0 < 0 || v0 < 0 || u1 > s.width || v1 > s.height || u0 >= u1 || v0 >= v1) return RSR_E_ARG;
+  if (s.batch > 65535) return RSR_E_ARG;
+  return launched(rsr::launch_road_roll(s.batch, s.height, s.width, u0, u1, v0, v1, disparity, out,
+                                        as_stream(stream)));
+}
+
 int rsr_reconstruct(rsr_shape s, rsr_rig rig, const float* disparity, float* xyz, void* stream) {
   if (!shape_ok(s) || !disparity || !xyz) return RSR_E_ARG;
   if (!(rig.f > 0) || !(rig.baseline > 0) || !(rig.d_min > 0)) return RSR_E_ARG;

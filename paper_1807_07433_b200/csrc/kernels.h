@@ -46,4 +46,13 @@ cudaError_t launch_reconstruct(int B, int H, int W, double f, double baseline, d
                                double v0, double d_min, const float* disp, float* xyz,
                                cudaStream_t st);
 
+// Road model (NEXT f3): RANSAC-LSF of d = alpha v + beta over grid samples of a
+// disparity map; model [B][3] = {alpha, beta, inliers}.
+size_t road_workspace_size(int B, int H, int W, int su, int sv, int n_hyp);
+cudaError_t launch_road_model(int B, int H, int W, int su, int sv, int n_hyp, float tol, unsigned seed,
+                              const float* disp, double* model, void* ws, cudaStream_t st);
+
+cudaError_t launch_road_roll(int B, int H, int W, int u0, int u1, int v0, int v1, const float* disp,
+                             double* out, cudaStream_t st);
+
 }  // namespace rsr

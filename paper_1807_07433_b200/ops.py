@@ -8,7 +8,8 @@ import math
 
 import torch
 
-from ._lib import (RsrAggParams, RsrCostParams, RsrDispParams, RsrRig, RsrShape, check, lib)
+from ._lib import (RsrAggParams, RsrCostParams, RsrDispParams, RsrRig, RsrRoadParams, RsrShape, check,
+                   lib)
 
 
 def _ptr(t):
@@ -135,6 +136,39 @@ def rsr_reconstruct(disparity, f, baseline, u0=None, v0=None, d_min=1.0, xyz=Non
     check("rsr_reconstruct", lib().rsr_reconstruct(
         RsrShape(B, H, W), RsrRig(f, baseline, u0, v0, d_min), _ptr(disparity), _ptr(xyz), _stream()))
     return xyz
+
+
+def rsr_road_model(disparity, step_u=4, step_v=4, n_hyp=512, inlier_tol=0.5, seed=0, model=None,
+                   workspace=None):
+    """Road model (Eq. 2): RANSAC-LSF of d = alpha v + beta over grid samples of
+    [B,H,W] disparity maps; returns float64 [B,3] = (alpha, beta, inliers)."""
+    if disparity.dim() == 2:
+        disparity = disparity.unsqueeze(0)
+    B, H, W = disparity.shape
+    _expect(disparity, torch.float32, (B, H, W), "disparity")
+    s = RsrShape(B, H, W)
+    p = RsrRoadParams(step_u, step_v, n_hyp, float(inlier_tol), seed & 0xFFFFFFFF)
+    dev = disparity.device
+    model = torch.empty((B, 3), dtype=torch.float64, device=dev) if model is None else model
+    nbytes = int(lib().rsr_road_workspace_size(s, p))
+    if workspace is None:
+        workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+    check("rsr_road_model", lib().rsr_road_model(s, p, _ptr(disparity), _ptr(model), _ptr(workspace),
+                                                 workspace.numel(), _stream()))
+    return model
+
+
+def rsr_road_roll(disparity, u0, u1, v0, v1, out=None):
+    """Roll angle: plane fit over the patch [v0,v1) x [u0,u1); float64 [B,5] =
+    (g0, g1, g2, gamma, n)."""
+    if disparity.dim() == 2:
+        disparity = disparity.unsqueeze(0)
+    B, H, W = disparity.shape
+    _expect(disparity, torch.float32, (B, H, W), "disparity")
+    out = torch.empty((B, 5), dtype=torch.float64, device=disparity.device) if out is None else out
+    check("rsr_road_roll", lib().rsr_road_roll(RsrShape(B, H, W), u0, u1, v0, v1, _ptr(disparity), _ptr(out),
+                                               _stream()))
+    return out
 
 
 _ = math  # (kept for callers that pass math.inf for gamma_r)

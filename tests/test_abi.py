@@ -60,5 +60,13 @@ def test_validation_without_gpu(L):
     assert L.rsr_disparity(s, RsrDispParams(0, 3, -1, 1), fake, fake, fake, fake, None, None, None) == 2
     assert L.rsr_reconstruct(s, RsrRig(0.0, 0.12, 0, 0, 1.0), fake, fake, None) == 2
     assert L.rsr_reconstruct(s, RsrRig(700.0, 0.12, 0, 0, 0.0), fake, fake, None) == 2
+    from paper_1807_07433_b200._lib import RsrRoadParams
+    rp = RsrRoadParams(4, 4, 64, 0.5, 0)
+    wsr = L.rsr_road_workspace_size(s, rp)
+    assert wsr > 0
+    assert L.rsr_road_model(s, RsrRoadParams(0, 4, 64, 0.5, 0), fake, fake, fake, wsr, None) == 2
+    assert L.rsr_road_model(s, RsrRoadParams(4, 4, 64, 0.0, 0), fake, fake, fake, wsr, None) == 2
+    assert L.rsr_road_model(s, rp, fake, fake, fake, wsr - 1, None) == 2
+    assert L.rsr_road_model(s, rp, None, fake, fake, wsr, None) == 2
     assert L.rsr_strerror(2) == b"invalid argument"
     assert L.rsr_version() >= 10000
