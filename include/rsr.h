@@ -85,8 +85,10 @@ int rsr_warp(rsr_shape s, const double* alpha_beta, const uint8_t* target,
 /* The two are bitwise consistent: vol_tar[v][u-r][k] == vol_ref[v][u][k].    */
 /* nan_ref / nan_tar (optional, uint8 [B][H][W]) summarise each pixel's D    */
 /* costs: bit 0 = some k is NaN, bit 1 = some k is finite (so 1 = all NaN,    */
-/* 3 = partly NaN).  rsr_aggregate uses them to skip per-disparity validity   */
-/* bookkeeping wherever no pixel of a tile is partly NaN.                     */
+/* 3 = partly NaN); for D <= 64 also bit 2 / bit 3 = some k in the low / high */
+/* half [0, H0) / [H0, D) is NaN, H0 = roundup8(D)/2, and bit 7 = bits 2-3   */
+/* present.  rsr_aggregate uses them to skip per-disparity validity          */
+/* bookkeeping wherever no pixel of a tile (or of a half) is partly NaN.     */
 /*   workspace : device scratch of rsr_cost_workspace_size(s) bytes, 16-byte  */
 /*               aligned, owned by the caller (per-pixel block sums / norms). */
 /* Errors: RSR_E_ARG on NULL ref/warped/valid/vol_ref/workspace, rho_block   */
@@ -117,7 +119,8 @@ int rsr_cost_volume(rsr_shape s, rsr_cost_params p, const uint8_t* ref,
 /*   vol     : float [B][H][W][D], NaN = invalid                              */
 /*   guide   : uint8 [B][H][W]                                                */
 /*   nan_map : optional uint8 [B][H][W] in the rsr_cost_volume encoding       */
-/*             (bit 0 some k NaN, bit 1 some k finite); it must describe vol  */
+/*             (bit 0 some k NaN, bit 1 some k finite; optionally bits 2-3    */
+/*             per disparity half with bit 7 set); it must describe vol       */
 /*             exactly.  NULL = assume any pixel may be partly NaN (correct,  */
 /*             slower).                                                       */
 /*   out     : float [B][H][W][D]; must not alias vol                         */

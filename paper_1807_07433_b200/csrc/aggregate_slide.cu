@@ -279,12 +279,74 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
   }
 }
 
+// One input row of the sliding accumulation: NT taps, each FFMA2-ing NQ cost pairs
+// into the 2 rho + 1 ages; the last tap shifts the ages and returns the completed
+// row in fin.  MODE 0: clean pairs (k, k+1) of 8 disparities (NQ = 4); MODE 1:
+// (cost or 0, validity) of 4 disparities (NQ = 4); MODE 2: (cost or 0) pairs of 4
+// disparities with the per-pixel denominator (a half whose pixels are all fully
+// valid or skipped, NQ = 2).
+template <int RHO, int MODE>
+RSR_DEVINL void slide_row(float2 (&acc)[2 * RHO + 1][4], float2 (&fin)[4], const float* crow,
+                          const float* wrow, int KS, int G) {
+  constexpr int NT = 2 * RHO + 1;
+  constexpr int NQ = MODE == 2 ? 2 : 4;
+#pragma unroll
+  for (int j = 0; j < NT; j++) {
+    float2 cp[4];
+    if (MODE == 0) {
+      const float4 ca = *reinterpret_cast<const float4*>(crow + j * KS);
+      const float4 cb = *reinterpret_cast<const float4*>(crow + j * KS + 4 * G);
+      cp[0] = make_float2(ca.x, ca.y); cp[1] = make_float2(ca.z, ca.w);
+      cp[2] = make_float2(cb.x, cb.y); cp[3] = make_float2(cb.z, cb.w);
+    } else {
+      const float4 t = *reinterpret_cast<const float4*>(crow + j * KS);
+      const float tv[4] = {t.x, t.y, t.z, t.w};
+      float c0[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) c0[q] = (tv[q] != tv[q]) ? 0.f : tv[q];
+      if (MODE == 1) {
+#pragma unroll
+        for (int q = 0; q < 4; q++) cp[q] = make_float2(c0[q], (tv[q] != tv[q]) ? 0.f : 1.f);
+      } else {
+        cp[0] = make_float2(c0[0], c0[1]);
+        cp[1] = make_float2(c0[2], c0[3]);
+      }
+    }
+    float wv[16];
+    const float4* w4 = reinterpret_cast<const float4*>(wrow + j * 16);
+#pragma unroll
+    for (int q = 0; q < (NT + 3) / 4; q++) {
+      const float4 t = w4[q];
+      wv[4 * q] = t.x; wv[4 * q + 1] = t.y; wv[4 * q + 2] = t.z; wv[4 * q + 3] = t.w;
+    }
+    // q outer, ages inner: the cost pair stays in the operand reuse cache for
+    // 2 rho + 1 consecutive FFMA2s, so each reads only the weight and the
+    // accumulator pair from the register file (2 reads per bank)
+    if (j < NT - 1) {
+#pragma unroll
+      for (int q = 0; q < NQ; q++)
+#pragma unroll
+        for (int a = 0; a < NT; a++) acc[a][q] = fma2s(wv[a], cp[q], acc[a][q]);
+    } else {
+      // last tap of the row: age 0 completes, every other age moves one slot down
+#pragma unroll
+      for (int q = 0; q < NQ; q++) {
+        fin[q] = fma2s(wv[0], cp[q], acc[0][q]);
+#pragma unroll
+        for (int a = 1; a < NT; a++) acc[a - 1][q] = fma2s(wv[a], cp[q], acc[a][q]);
+        acc[NT - 1][q] = make_float2(0.f, 0.f);
+      }
+    }
+  }
+}
+
 // ---- consumers (G warps): sliding accumulation, FFMA2 -----------------------
 template <int RHO, bool CLEAN>
 __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, const Seg& s,
                                         const float* cost_s, const float* w_s, uint64_t* full_c,
                                         uint64_t* empty_c, uint64_t* full_w, uint64_t* empty_w,
-                                        uint32_t& it, int xl, int l, int lane, const short* gt) {
+                                        uint32_t& it, int xl, int l, int lane, const short* gt,
+                                        int hcmask) {
   constexpr int NT = 2 * RHO + 1;
   constexpr int NPASS = CLEAN ? 1 : 2;
   const int NR = (s.yb - s.ya) + 2 * RHO;
@@ -329,6 +391,7 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
       for (int q = 0; q < 4; q++) acc[a][q] = make_float2(0.f, 0.f);
     // this lane's disparities: clean {4l..4l+3} U {4G+4l..}, general pass h: {4Gh + 4l..}
     const int koff = CLEAN ? 4 * l : 4 * g.G * pass + 4 * l;
+    const bool hc = !CLEAN && ((hcmask >> pass) & 1);   // this half has no partially-NaN pixel
     for (int i = 0; i < NR; i++, it++) {
       const int stc = it % SG_NSC, stw = it % SG_NSW;
       mbar_wait_parity(&full_c[stc], (it / SG_NSC) & 1);
@@ -336,50 +399,13 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
       const float* crow = cost_s + (size_t)stc * g.CX * g.KS + xl * g.KS + koff;
       const float* wrow = w_s + (size_t)stw * g.WST + xl * g.XS;
       float2 fin[4];
-#pragma unroll
-      for (int j = 0; j < NT; j++) {
-        float2 cp[4];
-        if (CLEAN) {
-          const float4 ca = *reinterpret_cast<const float4*>(crow + j * g.KS);
-          const float4 cb = *reinterpret_cast<const float4*>(crow + j * g.KS + 4 * g.G);
-          cp[0] = make_float2(ca.x, ca.y); cp[1] = make_float2(ca.z, ca.w);
-          cp[2] = make_float2(cb.x, cb.y); cp[3] = make_float2(cb.z, cb.w);
-        } else {
-          const float4 t = *reinterpret_cast<const float4*>(crow + j * g.KS);
-          const float tv[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const bool ok = !(tv[q] != tv[q]);
-            cp[q] = make_float2(ok ? tv[q] : 0.f, ok ? 1.f : 0.f);
-          }
-        }
-        float wv[16];
-        const float4* w4 = reinterpret_cast<const float4*>(wrow + j * 16);
-#pragma unroll
-        for (int q = 0; q < (NT + 3) / 4; q++) {
-          const float4 t = w4[q];
-          wv[4 * q] = t.x; wv[4 * q + 1] = t.y; wv[4 * q + 2] = t.z; wv[4 * q + 3] = t.w;
-        }
-        // q outer, ages inner: the cost pair stays in the operand reuse cache for
-        // 2 rho + 1 consecutive FFMA2s, so each reads only the weight and the
-        // accumulator pair from the register file (2 reads per bank)
-        if (j < NT - 1) {
-#pragma unroll
-          for (int q = 0; q < 4; q++)
-#pragma unroll
-            for (int a = 0; a < NT; a++) acc[a][q] = fma2s(wv[a], cp[q], acc[a][q]);
-        } else {
-          // last tap of the row: age 0 completes, every other age moves one slot down
-#pragma unroll
-          for (int q = 0; q < 4; q++) {
-            fin[q] = fma2s(wv[0], cp[q], acc[0][q]);
-#pragma unroll
-            for (int a = 1; a < NT; a++) acc[a - 1][q] = fma2s(wv[a], cp[q], acc[a][q]);
-            acc[NT - 1][q] = make_float2(0.f, 0.f);
-          }
-        }
-      }
-      const float den = CLEAN ? wrow[(32 - xl) * g.XS + xl] : 0.f;
+      if (CLEAN)
+        slide_row<RHO, 0>(acc, fin, crow, wrow, g.KS, g.G);
+      else if (hc)
+        slide_row<RHO, 2>(acc, fin, crow, wrow, g.KS, g.G);
+      else
+        slide_row<RHO, 1>(acc, fin, crow, wrow, g.KS, g.G);
+      const float den = (CLEAN || hc) ? wrow[(32 - xl) * g.XS + xl] : 0.f;
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&empty_c[stc]);
@@ -406,6 +432,13 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
                 if (kb + q < A.D) oh[q] = r[4 * hh + q];
             }
           }
+        } else if (hc) {
+          // fully valid half: same formula as the clean path (bitwise equal)
+          const float inv = __frcp_rn(den);
+          const float r[4] = {fin[0].x * inv, fin[0].y * inv, fin[1].x * inv, fin[1].y * inv};
+#pragma unroll
+          for (int q = 0; q < 4; q++)
+            if (s.k0 + koff + q < s.k0 + s.ks_eff) o[q] = r[q];
         } else {
           const float* cv = A.vol + pix * A.D + s.k0 + koff;
           const float fv[8] = {fin[0].x, fin[0].y, fin[1].x, fin[1].y, fin[2].x, fin[2].y, fin[3].x, fin[3].y};
@@ -462,6 +495,7 @@ __global__ void __launch_bounds__(384, 1) k_aggregate_slide(const SlideArgs A) {
     // nan_map byte: bit 0 = some disparity NaN, bit 1 = some disparity finite.  Only a
     // partially-NaN pixel (3) needs per-disparity denominators (the general path).
     int partial = (A.nan_map == nullptr) ? 1 : 0;
+    int dirty = (A.nan_map == nullptr) ? 3 : 0;
     const int rows = (s.yb - s.ya) + 4 * RHO;
     constexpr int UNR = 8;   // independent loads in flight per thread
     for (int e0 = tid; e0 < rows * g.CX; e0 += UNR * blockDim.x) {
@@ -483,13 +517,20 @@ __global__ void __launch_bounds__(384, 1) k_aggregate_slide(const SlideArgs A) {
         const int e = e0 + u * blockDim.x;
         if (e < rows * g.CX) {
           const int yy = s.ya - 2 * RHO + e / g.CX;
-          if (mv[u] == 3 && yy >= s.ya - RHO && yy < s.yb + RHO) partial = 1;
+          if ((mv[u] & 3) == 3 && yy >= s.ya - RHO && yy < s.yb + RHO) {
+            partial = 1;
+            // bits 2/3: NaN present in disparity half 0/1, valid when bit 7 is set
+            // (k_nan_maps, single-slab volumes); otherwise both halves are dirty
+            dirty |= ((mv[u] & 0x80) && g.nslab == 1) ? ((mv[u] >> 2) & 3) : 3;
+          }
           // +inf marks a skipped pixel (outside the image or all-NaN)
-          gt[e] = mv[u] == 1 ? SG_GSKIP : (short)gv[u];
+          gt[e] = (mv[u] & 3) == 1 ? SG_GSKIP : (short)gv[u];
         }
       }
     }
     const bool clean = !__syncthreads_or(partial);
+    // pass h of the general path is "half-clean" when no partial pixel has NaN in half h
+    const int hcmask = (__syncthreads_or(dirty & 1) ? 0 : 1) | (__syncthreads_or(dirty & 2) ? 0 : 2);
     const int npass = clean ? 1 : 2;
     if (warp >= n_cons) {
       produce_weights<RHO>(A, g, s, clean, npass, gt, w_s, dpart, cost_s, full_w, empty_w, full_c, empty_c,
@@ -497,9 +538,9 @@ __global__ void __launch_bounds__(384, 1) k_aggregate_slide(const SlideArgs A) {
     } else {
       const int t = tid;   // consumer thread: column t / G, lane-in-group t % G
       if (clean)
-        consume<RHO, true>(A, g, s, cost_s, w_s, full_c, empty_c, full_w, empty_w, it, t / g.G, t % g.G, lane, gt);
+        consume<RHO, true>(A, g, s, cost_s, w_s, full_c, empty_c, full_w, empty_w, it, t / g.G, t % g.G, lane, gt, hcmask);
       else
-        consume<RHO, false>(A, g, s, cost_s, w_s, full_c, empty_c, full_w, empty_w, it, t / g.G, t % g.G, lane, gt);
+        consume<RHO, false>(A, g, s, cost_s, w_s, full_c, empty_c, full_w, empty_w, it, t / g.G, t % g.G, lane, gt, hcmask);
     }
   }
 }

@@ -495,15 +495,28 @@ __global__ void __launch_bounds__(256) k_nan_maps(int H, int W, int d_lo, int D,
     bcol = min(bcol, W - 1);
     return bcol < a ? 0 : cnt[bcol + 1] - cnt[a];
   };
+  // disparity halves of a single-slab volume (rsr_aggregate's two general passes):
+  // [0, H0) and [H0, D) with H0 = roundup8(D) / 2; bits 2 / 3 flag a NaN in each,
+  // bit 7 says the half bits are present
+  const bool halves = D <= 64;
+  const int H0 = ((D + 7) & ~7) / 2;
   for (int u = threadIdx.x; u < W; u += blockDim.x) {
     const bool lok = cL[u + 1] - cL[u] != 0, wok = cW[u + 1] - cW[u] != 0;
-    if (nan_ref) {
-      const int fin = lok ? count(cW, u - (d_lo + D - 1), u - d_lo) : 0;
-      nan_ref[row + u] = (uint8_t)((fin < D ? 1 : 0) | (fin > 0 ? 2 : 0));
+    if (nan_ref) {   // k valid iff inv_L(u) and inv_W(u - d_lo - k) finite
+      const int f0 = lok ? count(cW, u - d_lo - (H0 - 1), u - d_lo) : 0;
+      const int f1 = lok ? count(cW, u - d_lo - (D - 1), u - d_lo - H0) : 0;
+      const int fin = f0 + f1;
+      int m = (fin < D ? 1 : 0) | (fin > 0 ? 2 : 0);
+      if (halves) m |= (f0 < H0 ? 4 : 0) | (f1 < D - H0 ? 8 : 0) | 0x80;
+      nan_ref[row + u] = (uint8_t)m;
     }
-    if (nan_tar) {
-      const int fin = wok ? count(cL, u + d_lo, u + d_lo + D - 1) : 0;
-      nan_tar[row + u] = (uint8_t)((fin < D ? 1 : 0) | (fin > 0 ? 2 : 0));
+    if (nan_tar) {   // k valid iff inv_W(u') and inv_L(u' + d_lo + k) finite
+      const int f0 = wok ? count(cL, u + d_lo, u + d_lo + H0 - 1) : 0;
+      const int f1 = wok ? count(cL, u + d_lo + H0, u + d_lo + D - 1) : 0;
+      const int fin = f0 + f1;
+      int m = (fin < D ? 1 : 0) | (fin > 0 ? 2 : 0);
+      if (halves) m |= (f0 < H0 ? 4 : 0) | (f1 < D - H0 ? 8 : 0) | 0x80;
+      nan_tar[row + u] = (uint8_t)m;
     }
   }
 }

@@ -148,10 +148,15 @@ def test_parity_full_frame(rsr, name):
     ora = O.run_pipeline(f.left, f.right, f.alpha, f.beta, cfg)
     rep = compare(gpu, ora, (0, cfg.height), cfg, label=name)
     print(name, rep)
-    # nan maps: bit 0 = some k NaN, bit 1 = some k finite (include/rsr.h)
+    # nan maps: bit 0 = some k NaN, bit 1 = some k finite, bits 2 / 3 = some k NaN
+    # in the low / high disparity half, bit 7 = half bits present (include/rsr.h)
+    D = cfg.D
+    h0 = ((D + 7) & ~7) // 2
     for key, vk in (("nan_ref", "cost_ref"), ("nan_tar", "cost_tar")):
-        v = gpu[vk][0]
-        expect = np.isnan(v).any(axis=-1).astype(np.uint8) | (2 * (~np.isnan(v)).any(axis=-1)).astype(np.uint8)
+        v = np.isnan(gpu[vk][0])
+        expect = (v.any(axis=-1).astype(np.uint8) | (2 * (~v).any(axis=-1)).astype(np.uint8)
+                  | (4 * v[..., :h0].any(axis=-1)).astype(np.uint8)
+                  | (8 * v[..., h0:].any(axis=-1)).astype(np.uint8) | np.uint8(0x80))
         assert np.array_equal(gpu[key][0], expect)
 
 
