@@ -37,6 +37,7 @@
 //    accumulates numerator and per-disparity denominator, two passes per slab.
 //    Both accumulate in the same order, so they agree bitwise where both apply.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -301,13 +302,16 @@ RSR_DEVINL void slide_row(float2 (&acc)[2 * RHO + 1][4], float2 (&fin)[4], const
     } else {
       const float4 t = *reinterpret_cast<const float4*>(crow + j * KS);
       const float tv[4] = {t.x, t.y, t.z, t.w};
-      float c0[4];
-#pragma unroll
-      for (int q = 0; q < 4; q++) c0[q] = (tv[q] != tv[q]) ? 0.f : tv[q];
       if (MODE == 1) {
 #pragma unroll
-        for (int q = 0; q < 4; q++) cp[q] = make_float2(c0[q], (tv[q] != tv[q]) ? 0.f : 1.f);
+        for (int q = 0; q < 4; q++) {
+          const bool ok = !(tv[q] != tv[q]);
+          cp[q] = make_float2(ok ? tv[q] : 0.f, ok ? 1.f : 0.f);
+        }
       } else {
+        float c0[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) c0[q] = (tv[q] != tv[q]) ? 0.f : tv[q];
         cp[0] = make_float2(c0[0], c0[1]);
         cp[1] = make_float2(c0[2], c0[3]);
       }
@@ -391,7 +395,9 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
       for (int q = 0; q < 4; q++) acc[a][q] = make_float2(0.f, 0.f);
     // this lane's disparities: clean {4l..4l+3} U {4G+4l..}, general pass h: {4Gh + 4l..}
     const int koff = CLEAN ? 4 * l : 4 * g.G * pass + 4 * l;
-    const bool hc = !CLEAN && ((hcmask >> pass) & 1);   // this half has no partially-NaN pixel
+    // this half has no partially-NaN pixel (not used at rho = 7, where the extra code
+    // path would push the 120 accumulators into spills)
+    const bool hc = !CLEAN && RHO < 7 && ((hcmask >> pass) & 1);
     for (int i = 0; i < NR; i++, it++) {
       const int stc = it % SG_NSC, stw = it % SG_NSW;
       mbar_wait_parity(&full_c[stc], (it / SG_NSC) & 1);
@@ -577,6 +583,10 @@ static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, flo
     const long long ctas = cols * ((H + R - 1) / R);
     const double cost = (double)((ctas + nsm - 1) / nsm) * (R + 2 * RHO);
     if (cost < best * 0.999) { best = cost; bestR = R; }
+  }
+  if (const char* e = getenv("RSR_K3_ROWS")) {   // experiment hook (tools/): force R
+    const int r = atoi(e);
+    if (r >= 8 && r <= SG_SEGMAX) bestR = r;
   }
   A.R = bestR;
   A.nstrips = nstrips;
