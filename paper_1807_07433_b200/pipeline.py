@@ -65,6 +65,7 @@ class StereoPipeline:
         self.wta_tar = e((B, H, W), torch.int16)
         self.xyz = e((B, H, W, 3), torch.float32)
         self.workspace = e((ops.cost_workspace_bytes(B, H, W),), torch.uint8)
+        self._side = None
 
     def run(self, left, right, alpha_beta, with_wta=True):
         p = self.p
@@ -72,9 +73,21 @@ class StereoPipeline:
         ops.rsr_cost_volume(left, self.warped, self.valid, p.rho_block, p.d_lo, p.d_hi,
                             vol_ref=self.vol_ref, vol_tar=self.vol_tar, nan_ref=self.nan_ref,
                             nan_tar=self.nan_tar, workspace=self.workspace)
+        # the two aggregations are independent: the target volume's on a side stream, so
+        # each launch back-fills the other's last wave
+        main = torch.cuda.current_stream()
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=main.device)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        self._side.wait_event(fork)
+        with torch.cuda.stream(self._side):
+            ops.rsr_aggregate(self.vol_tar, self.warped, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_tar,
+                              self.agg_tar)
         ops.rsr_aggregate(self.vol_ref, left, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_ref, self.agg_ref)
-        ops.rsr_aggregate(self.vol_tar, self.warped, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_tar,
-                          self.agg_tar)
+        join = torch.cuda.Event()
+        join.record(self._side)
+        main.wait_event(join)
         ops.rsr_disparity(self.agg_ref, self.agg_tar, self.shift, p.d_lo, p.d_hi, p.lrc_tol, p.subpixel,
                           self.disparity, self.wta_ref if with_wta else None,
                           self.wta_tar if with_wta else None)
