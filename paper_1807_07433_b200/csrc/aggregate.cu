@@ -306,16 +306,20 @@ __global__ void k_fill_i16(long long n, int16_t v, int16_t* __restrict__ p) {
 
 cudaError_t launch_aggregate(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r,
                              const float* vol, const uint8_t* guide, const uint8_t* nan_map,
-                             float* out, int16_t* wta_k, float* wta_v, cudaStream_t st) {
-  if (rho <= 7)
-    return launch_aggregate_slide(B, H, W, D, rho, gamma_d, gamma_r, vol, guide, nan_map, out, wta_k, wta_v,
+                             float* out, int16_t* wta_k, cudaStream_t st) {
+  if (rho < 7)
+    return launch_aggregate_slide(B, H, W, D, rho, gamma_d, gamma_r, vol, guide, nan_map, out, wta_k,
                                   st);
-  if (wta_k) {   // the tiled variant computes no WTA: every pixel says "scan the volume"
+  // rho = 7 (no registers left for the epilogue's WTA) and the tiled variant compute no
+  // WTA: every pixel says "scan the volume"
+  if (wta_k) {
     const long long n = (long long)B * H * W;
     k_fill_i16<<<(int)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, st>>>(n, (int16_t)-2, wta_k);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
+  if (rho == 7)
+    return launch_aggregate_slide(B, H, W, D, rho, gamma_d, gamma_r, vol, guide, nan_map, out, nullptr, st);
 #define RSR_A(R) \
   case R: return aggregate_launch_t<R>(B, H, W, D, gamma_d, gamma_r, vol, guide, nan_map, out, st);
   switch (rho) {

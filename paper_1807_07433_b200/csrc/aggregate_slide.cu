@@ -113,7 +113,6 @@ struct SlideArgs {
   const uint8_t* nan_map;
   float* out;
   int16_t* wta_k;        // optional: per-pixel WTA of the aggregated volume (k; -1 none; -2 not computed here)
-  float* wta_v;          // optional: [3] per pixel: A[k-1], A[k], A[k+1] (NaN outside / invalid)
 };
 
 // The CTA's segment.  The 1-D grid enumerates (strip rank, row chunk, frame x
@@ -378,7 +377,6 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
         if (A.wta_k && y >= s.ya && x < A.W && l == 0 && pass == 0) {   // all-NaN pixels: no WTA
           const size_t pix = s.pix0 + (size_t)y * A.W + x;
           A.wta_k[pix] = -1;
-          A.wta_v[3 * pix] = A.wta_v[3 * pix + 1] = A.wta_v[3 * pix + 2] = qnan();
         }
         if (y >= s.ya && x < A.W) {
           float* o = A.out + (s.pix0 + (size_t)y * A.W + x) * A.D + s.k0 + koff;
@@ -429,53 +427,26 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
       const float inv = CLEAN ? __frcp_rn(den) : 0.f;
       const float r[8] = {fin[0].x * inv, fin[0].y * inv, fin[1].x * inv, fin[1].y * inv,
                           fin[2].x * inv, fin[2].y * inv, fin[3].x * inv, fin[3].y * inv};
-      if (A.wta_k && y >= s.ya) {
-        // WTA of the completed row for rsr_disparity_maps (same values as written below):
-        // the G lanes of a pixel hold its KS disparities; lane-local max-then-first-index,
-        // then an xor reduction over the group (power-of-two G, one slab); the general
-        // path leaves -2 ("scan the volume").
+      if (RHO < 7 && A.wta_k && y >= s.ya) {   // rho = 7: the host fills -2
+        // WTA of the completed row for rsr_disparity_maps (the values written below): the
+        // G lanes of a pixel hold its KS disparities.  Max over the group (NaN = missing),
+        // then the lowest k holding it -- k_disparity's "first strict maximum above -inf".
+        // The general path leaves -2 ("scan the volume").
         const size_t pix = s.pix0 + (size_t)y * A.W + x;
         if (CLEAN && g.nslab == 1 && (g.G & (g.G - 1)) == 0) {
           float rv[8];
 #pragma unroll
-          for (int q = 0; q < 8; q++) {
-            const int k = koff + (q < 4 ? q : 4 * g.G + q - 4);
-            rv[q] = k < A.D ? r[q] : qnan();
-          }
-          float m = rv[0];
+          for (int q = 0; q < 8; q++) rv[q] = koff + (q < 4 ? q : 4 * g.G + q - 4) < A.D ? r[q] : qnan();
+          float m = -INFINITY;
 #pragma unroll
-          for (int q = 1; q < 8; q++) m = fmaxf(m, rv[q]);
-          int kb = -1;
+          for (int q = 0; q < 8; q++) m = fmaxf(m, rv[q]);
+          for (int o = g.G >> 1; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+          int kb = 0x7fff;
 #pragma unroll
           for (int q = 7; q >= 0; q--)
             if (rv[q] == m) kb = koff + (q < 4 ? q : 4 * g.G + q - 4);
-          for (int o = g.G >> 1; o >= 1; o >>= 1) {
-            const float om = __shfl_xor_sync(0xffffffffu, m, o);
-            const int ok = __shfl_xor_sync(0xffffffffu, kb, o);
-            if (ok >= 0 && (kb < 0 || om > m || (om == m && ok < kb))) { m = om; kb = ok; }
-          }
-          // A[kb -/+ 1] from the lanes that hold them (the slot is uniform in the group)
-          const int gbase = lane - l;
-          float nb[2];
-#pragma unroll
-          for (int t = 0; t < 2; t++) {
-            const int k = kb + (t == 0 ? -1 : 1);
-            const bool in = kb >= 0 && k >= 0 && k < A.D;
-            const int kk = in ? k : 0;
-            const int half = kk / (4 * g.G), w = kk % (4 * g.G);
-            const int slot = (w & 3) + 4 * half;
-            float sel = rv[0];
-#pragma unroll
-            for (int q = 1; q < 8; q++) sel = slot == q ? rv[q] : sel;
-            const float got = __shfl_sync(0xffffffffu, sel, gbase + (w >> 2));
-            nb[t] = in ? got : qnan();
-          }
-          if (l == 0 && x < A.W) {
-            A.wta_k[pix] = (int16_t)kb;
-            A.wta_v[3 * pix] = nb[0];
-            A.wta_v[3 * pix + 1] = kb >= 0 ? m : qnan();
-            A.wta_v[3 * pix + 2] = nb[1];
-          }
+          for (int o = g.G >> 1; o >= 1; o >>= 1) kb = min(kb, __shfl_xor_sync(0xffffffffu, kb, o));
+          if (l == 0 && x < A.W) A.wta_k[pix] = (int16_t)(m > -INFINITY ? kb : -1);
         } else if (l == 0 && x < A.W) {
           A.wta_k[pix] = -2;
         }
@@ -622,7 +593,7 @@ static int sm_count() {
 template <int RHO>
 static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, float gamma_r,
                                   const float* vol, const uint8_t* guide, const uint8_t* nan_map,
-                                  float* out, int16_t* wta_k, float* wta_v, cudaStream_t st) {
+                                  float* out, int16_t* wta_k, cudaStream_t st) {
   const SlideGeom g = slide_geom(D, RHO);
   auto kern = k_aggregate_slide<RHO>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.bytes);
@@ -652,7 +623,7 @@ static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, flo
   A.kd = -log2e / (gamma_d * gamma_d);
   A.kr = std::isinf(gamma_r) ? -1e-30f : -log2e / (gamma_r * gamma_r);
   A.vol = vol; A.guide = guide; A.nan_map = nan_map; A.out = out;
-  A.wta_k = wta_k; A.wta_v = wta_v;
+  A.wta_k = wta_k;
   const long long nblk = cols * ((H + bestR - 1) / bestR);
   if (nblk > 0x7fffffffLL) return cudaErrorInvalidValue;
   kern<<<(unsigned)nblk, 32 * (g.G + SG_NPROD), g.bytes, st>>>(A);
@@ -663,9 +634,9 @@ size_t aggregate_slide_smem(int D, int rho, int H) { (void)H; return slide_geom(
 
 cudaError_t launch_aggregate_slide(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r,
                                    const float* vol, const uint8_t* guide, const uint8_t* nan_map,
-                                   float* out, int16_t* wta_k, float* wta_v, cudaStream_t st) {
+                                   float* out, int16_t* wta_k, cudaStream_t st) {
 #define RSR_S(R) \
-  case R: return slide_launch_t<R>(B, H, W, D, gamma_d, gamma_r, vol, guide, nan_map, out, wta_k, wta_v, st);
+  case R: return slide_launch_t<R>(B, H, W, D, gamma_d, gamma_r, vol, guide, nan_map, out, wta_k, st);
   switch (rho) {
     RSR_S(0) RSR_S(1) RSR_S(2) RSR_S(3) RSR_S(4) RSR_S(5) RSR_S(6) RSR_S(7)
     default:

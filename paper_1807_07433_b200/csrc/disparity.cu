@@ -144,10 +144,11 @@ __global__ void __launch_bounds__(256) k_disparity(int H, int W, int d_lo, int D
   }
 }
 
-// From the WTA maps of rsr_aggregate: k and A[k-1..k+1] per pixel are read from
-// the maps; a pixel whose map says -2 (not computed by the aggregation: general
-// path, tiled variant) is scanned from its volume row exactly like k_disparity,
-// so the results are bitwise those of k_disparity.  One thread per pixel.
+// From the WTA maps of rsr_aggregate: k per pixel is read from the maps; a pixel
+// whose map says -2 (not computed by the aggregation: general path, tiled
+// variant) is scanned from its volume row exactly like k_disparity, so the
+// results are bitwise those of k_disparity.  Kept pixels read A[k-1..k+1] for
+// the parabola (12 bytes instead of the D-float row).  One thread per pixel.
 RSR_DEVINL int argmax_scan(const float* __restrict__ p, int D) {
   float best = -INFINITY;
   int kb = -1;
@@ -162,7 +163,6 @@ __global__ void __launch_bounds__(256) k_disparity_maps(int H, int W, int d_lo, 
                                                         const float* __restrict__ agg_ref,
                                                         const float* __restrict__ agg_tar,
                                                         const int16_t* __restrict__ kref,
-                                                        const float* __restrict__ vref,
                                                         const int16_t* __restrict__ ktar,
                                                         const int32_t* __restrict__ shift,
                                                         float* __restrict__ disp) {
@@ -178,18 +178,8 @@ __global__ void __launch_bounds__(256) k_disparity_maps(int H, int W, int d_lo, 
   const float sv = (float)shift[(size_t)b * H + v];
   for (int u = threadIdx.x; u < W; u += blockDim.x) {
     int k = kref[row + u];
-    float a, bb, c;
-    if (k == -2) {
-      const float* p = agg_ref + (row + u) * D;
-      k = argmax_scan(p, D);
-      a = (k >= 1) ? p[k - 1] : qnan();
-      bb = (k >= 0) ? p[k] : qnan();
-      c = (k >= 0 && k + 1 < D) ? p[k + 1] : qnan();
-    } else {
-      a = vref[3 * (row + u)];
-      bb = vref[3 * (row + u) + 1];
-      c = vref[3 * (row + u) + 2];
-    }
+    const float* p = agg_ref + (row + u) * D;
+    if (k == -2) k = argmax_scan(p, D);
     float d = qnan();
     if (k >= 0) {
       const int up = u - (k + d_lo);
@@ -198,6 +188,8 @@ __global__ void __launch_bounds__(256) k_disparity_maps(int H, int W, int d_lo, 
         if (kr >= 0 && abs(k - kr) <= tol) {
           float r = (float)(k + d_lo);
           if (subpix && k >= 1 && k <= D - 2) {
+            // the three values around the winner: one or two sectors of this pixel's row
+            const float a = __ldg(p + k - 1), bb = __ldg(p + k), c = __ldg(p + k + 1);
             const float den = 2.f * a + 2.f * c - 4.f * bb;
             if (!(a != a) && !(c != c) && fabsf(den) > 1e-12f) r += __fdiv_rn(a - c, den);
           }
@@ -211,7 +203,7 @@ __global__ void __launch_bounds__(256) k_disparity_maps(int H, int W, int d_lo, 
 
 cudaError_t launch_disparity_maps(int B, int H, int W, int d_lo, int D, int tol, int subpix,
                                   const float* agg_ref, const float* agg_tar, const int16_t* kref,
-                                  const float* vref, const int16_t* ktar, const int32_t* shift,
+                                  const int16_t* ktar, const int32_t* shift,
                                   float* disp, cudaStream_t st) {
   const size_t smem = sizeof(int16_t) * (size_t)W;
   if (smem > 48 * 1024) {
@@ -219,7 +211,7 @@ cudaError_t launch_disparity_maps(int B, int H, int W, int d_lo, int D, int tol,
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  k_disparity_maps<<<dim3(H, B), 256, smem, st>>>(H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, kref, vref,
+  k_disparity_maps<<<dim3(H, B), 256, smem, st>>>(H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, kref,
                                                   ktar, shift, disp);
   return cudaGetLastError();
 }

@@ -68,8 +68,6 @@ class StereoPipeline:
         # per-pixel winner-take-all maps written by the aggregations (rsr_disparity_maps)
         self.wk_ref = e((B, H, W), torch.int16)
         self.wk_tar = e((B, H, W), torch.int16)
-        self.wv_ref = e((B, H, W, 3), torch.float32)
-        self.wv_tar = e((B, H, W, 3), torch.float32)
         self._side = None
 
     def run(self, left, right, alpha_beta, with_wta=True):
@@ -88,15 +86,15 @@ class StereoPipeline:
         self._side.wait_event(fork)
         with torch.cuda.stream(self._side):
             ops.rsr_aggregate(self.vol_tar, self.warped, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_tar,
-                              self.agg_tar, wta_k=self.wk_tar, wta_v=self.wv_tar)
+                              self.agg_tar, wta_k=self.wk_tar)
         ops.rsr_aggregate(self.vol_ref, left, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_ref, self.agg_ref,
-                          wta_k=self.wk_ref, wta_v=self.wv_ref)
+                          wta_k=self.wk_ref)
         join = torch.cuda.Event()
         join.record(self._side)
         main.wait_event(join)
         # steps 4-5 from the aggregations' WTA maps (bitwise equal to rsr_disparity, which
         # re-reads both volumes); with_wta also fills the full k maps via rsr_disparity
-        ops.rsr_disparity_maps(self.agg_ref, self.agg_tar, self.wk_ref, self.wv_ref, self.wk_tar, self.shift,
+        ops.rsr_disparity_maps(self.agg_ref, self.agg_tar, self.wk_ref, self.wk_tar, self.shift,
                                p.d_lo, p.d_hi, p.lrc_tol, p.subpixel, self.disparity)
         if with_wta:
             ops.rsr_disparity(self.agg_ref, self.agg_tar, self.shift, p.d_lo, p.d_hi, p.lrc_tol, p.subpixel,

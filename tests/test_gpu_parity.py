@@ -308,9 +308,9 @@ def test_bad_arguments_return_codes(rsr):
     L = lib()
     x = torch.zeros(16, device="cuda")
     p = x.data_ptr()
-    assert L.rsr_aggregate(RsrShape(1, 2, 2), 4, RsrAggParams(-1, 1.0, 1.0), p, p, None, p + 64, None, None, None) == 2
-    assert L.rsr_aggregate(RsrShape(1, 2, 2), 4, RsrAggParams(1, 0.0, 1.0), p, p, None, p + 64, None, None, None) == 2
-    assert L.rsr_aggregate(RsrShape(1, 2, 2), 4, RsrAggParams(1, 1.0, 1.0), p, p, None, p, None, None, None) == 2
+    assert L.rsr_aggregate(RsrShape(1, 2, 2), 4, RsrAggParams(-1, 1.0, 1.0), p, p, None, p + 64, None, None) == 2
+    assert L.rsr_aggregate(RsrShape(1, 2, 2), 4, RsrAggParams(1, 0.0, 1.0), p, p, None, p + 64, None, None) == 2
+    assert L.rsr_aggregate(RsrShape(1, 2, 2), 4, RsrAggParams(1, 1.0, 1.0), p, p, None, p, None, None) == 2
 
 
 @pytest.mark.parametrize("name,case", [("c1", None), ("c2", None), ("c5x2", None), ("edge", "rho7_D96"),
@@ -337,24 +337,15 @@ def test_disparity_from_wta_maps_bitwise(rsr, name, case):
     B, H, W = L.shape
     kl = torch.empty((B, H, W), dtype=torch.int16, device="cuda")
     kr = torch.empty_like(kl)
-    vl = torch.empty((B, H, W, 3), dtype=torch.float32, device="cuda")
-    vr = torch.empty_like(vl)
-    al = rsr.rsr_aggregate(cl, L, cfg.rho_agg, cfg.gamma_d, cfg.gamma_r, nl, wta_k=kl, wta_v=vl)
-    ar = rsr.rsr_aggregate(cr, W_, cfg.rho_agg, cfg.gamma_d, cfg.gamma_r, nr, wta_k=kr, wta_v=vr)
+    al = rsr.rsr_aggregate(cl, L, cfg.rho_agg, cfg.gamma_d, cfg.gamma_r, nl, wta_k=kl)
+    ar = rsr.rsr_aggregate(cr, W_, cfg.rho_agg, cfg.gamma_d, cfg.gamma_r, nr, wta_k=kr)
     d0, k0l, k0r = rsr.rsr_disparity(al, ar, S_, cfg.d_lo, cfg.d_hi, cfg.lrc_tol, True, with_wta=True)
-    d1 = rsr.rsr_disparity_maps(al, ar, kl, vl, kr, S_, cfg.d_lo, cfg.d_hi, cfg.lrc_tol, True)
+    d1 = rsr.rsr_disparity_maps(al, ar, kl, kr, S_, cfg.d_lo, cfg.d_hi, cfg.lrc_tol, True)
     torch.cuda.synchronize()
     assert torch.equal(torch.nan_to_num(d0, nan=-7.0), torch.nan_to_num(d1, nan=-7.0))
     for k_map, k_ref in ((kl, k0l), (kr, k0r)):
         done = k_map != -2
         assert torch.equal(k_map[done], k_ref[done])
-    # the values beside the winner are the volume's
-    done = (kl >= 0)
-    if done.any():
-        D = cfg.D
-        idx = kl.clamp(min=0).long()
-        for t, off in ((0, -1), (1, 0), (2, 1)):
-            kk = idx + off
-            ok = done & (kk >= 0) & (kk < D)
-            vol_v = torch.gather(al, 3, kk.clamp(0, D - 1).unsqueeze(-1)).squeeze(-1)
-            assert torch.equal(torch.nan_to_num(vl[..., t][ok], nan=-7.0), torch.nan_to_num(vol_v[ok], nan=-7.0))
+    if name in ("c2", "c5x2"):
+        # the frame workloads take the epilogue's WTA for most pixels (not the scan)
+        assert (kl == -2).float().mean().item() < 0.5 and (kr == -2).float().mean().item() < 0.5
