@@ -229,15 +229,14 @@ def main():
         fork = torch.cuda.Event(); fork.record(stream); side.wait_event(fork)
         with torch.cuda.stream(side):
             rsr.rsr_aggregate(pipe.vol_tar, pipe.warped, p.rho_agg, p.gamma_d, p.gamma_r, pipe.nan_tar,
-                              pipe.agg_tar, wta_k=pipe.wk_tar)
-        rsr.rsr_aggregate(pipe.vol_ref, L, p.rho_agg, p.gamma_d, p.gamma_r, pipe.nan_ref, pipe.agg_ref,
-                          wta_k=pipe.wk_ref)
+                              pipe.agg_tar)
+        rsr.rsr_aggregate(pipe.vol_ref, L, p.rho_agg, p.gamma_d, p.gamma_r, pipe.nan_ref, pipe.agg_ref)
         join = torch.cuda.Event(); join.record(side); stream.wait_event(join)
         if record:
             e = torch.cuda.Event(enable_timing=True); e.record(stream); ev["agg3"].append(e)
             e = torch.cuda.Event(enable_timing=True); e.record(stream); ev["disp0"].append(e)
-        rsr.rsr_disparity_maps(pipe.agg_ref, pipe.agg_tar, pipe.wk_ref, pipe.wk_tar, pipe.shift,
-                               p.d_lo, p.d_hi, p.lrc_tol, True, pipe.disparity)
+        rsr.rsr_disparity(pipe.agg_ref, pipe.agg_tar, pipe.shift, p.d_lo, p.d_hi, p.lrc_tol, True,
+                          pipe.disparity)
         if record:
             e = torch.cuda.Event(enable_timing=True); e.record(stream); ev["disp1"].append(e)
         rsr.rsr_reconstruct(pipe.disparity, p.focal, p.baseline, d_min=p.d_min, xyz=pipe.xyz)

@@ -124,13 +124,6 @@ int rsr_cost_volume(rsr_shape s, rsr_cost_params p, const uint8_t* ref,
 /*             exactly.  NULL = assume any pixel may be partly NaN (correct,  */
 /*             slower).                                                       */
 /*   out     : float [B][H][W][D]; must not alias vol                         */
-/*   wta_k   : optional int16 [B][H][W] out: per-pixel winner-take-all of out */
-/*             for rsr_disparity_maps = smallest k maximising out over       */
-/*             entries > -inf (-1 if none), or -2 where this call did not     */
-/*             compute it (general-path tiles, rho >= 7, D > 64, lane groups  */
-/*             that are not a power of two).  Taken in the aggregation        */
-/*             epilogue from the values written to out, so the disparity     */
-/*             step need not re-read the volume.  NULL = not written.        */
 /* Errors: RSR_E_ARG on NULL vol/guide/out, D < 1 or > 32767, rho < 0 or      */
 /* > 10, gamma_d <= 0 or NaN, gamma_r <= 0 or NaN.                            */
 typedef struct {
@@ -141,7 +134,7 @@ typedef struct {
 
 int rsr_aggregate(rsr_shape s, int32_t D, rsr_agg_params p, const float* vol,
                   const uint8_t* guide, const uint8_t* nan_map, float* out,
-                  int16_t* wta_k, void* stream);
+                  void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Steps 4-5 — WTA, left-right consistency, parabola subpixel and            */
@@ -169,16 +162,6 @@ typedef struct {
 int rsr_disparity(rsr_shape s, rsr_disp_params p, const float* agg_ref,
                   const float* agg_tar, const int32_t* shift, float* disparity,
                   int16_t* wta_ref, int16_t* wta_tar, void* stream);
-
-/* The same steps from the WTA maps rsr_aggregate wrote for both volumes:     */
-/* k_L and k_R are read from the maps (pixels whose map says -2 are scanned   */
-/* from agg_ref / agg_tar); agg_ref[k_L-1..k_L+1] is read for the parabola of  */
-/* kept pixels only.  Bitwise the same disparity as rsr_disparity on the same */
-/* volumes.  Errors: as rsr_disparity, plus NULL maps.                        */
-int rsr_disparity_maps(rsr_shape s, rsr_disp_params p, const float* agg_ref,
-                       const float* agg_tar, const int16_t* wta_ref_k,
-                       const int16_t* wta_tar_k,
-                       const int32_t* shift, float* disparity, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Step 5b — triangulation (the paper gives no formula: rectified  */

@@ -6,7 +6,7 @@ plumbing (pipeline.py).  PyTorch supplies device memory, streams and
 torch.distributed only.
 """
 from ._lib import RsrError, lib  # noqa: F401
-from .ops import (rsr_aggregate, rsr_cost_volume, rsr_disparity, rsr_disparity_maps, rsr_reconstruct,  # noqa: F401
+from .ops import (rsr_aggregate, rsr_cost_volume, rsr_disparity, rsr_reconstruct,  # noqa: F401
                   rsr_warp, rsr_road_model, rsr_road_roll,
                   cost_workspace_bytes)
 from .pipeline import StereoParams, StereoPipeline  # noqa: F401

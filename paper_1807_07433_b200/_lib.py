@@ -62,9 +62,7 @@ def lib() -> ctypes.CDLL:
         L.rsr_cost_workspace_size.argtypes = [RsrShape]
         L.rsr_cost_workspace_size.restype = ctypes.c_size_t
         L.rsr_cost_volume.argtypes = [RsrShape, RsrCostParams, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]
-        L.rsr_aggregate.argtypes = [RsrShape, ctypes.c_int32, RsrAggParams, P, P, P, P, P, P]
-        L.rsr_disparity_maps.argtypes = [RsrShape, RsrDispParams, P, P, P, P, P, P, P]
-        L.rsr_disparity_maps.restype = ctypes.c_int
+        L.rsr_aggregate.argtypes = [RsrShape, ctypes.c_int32, RsrAggParams, P, P, P, P, P]
         L.rsr_disparity.argtypes = [RsrShape, RsrDispParams, P, P, P, P, P, P, P]
         L.rsr_reconstruct.argtypes = [RsrShape, RsrRig, P, P, P]
         L.rsr_road_workspace_size.argtypes = [RsrShape, RsrRoadParams]

@@ -27,7 +27,6 @@
 //    pair = (C0, V) with C0 = cost or 0, V = validity, so the same FFMA2 loop
 //    accumulates numerator and per-disparity denominator; two passes cover
 //    the 16 disparities.
-#include <algorithm>
 #include <cmath>
 
 #include "common.cuh"
@@ -299,27 +298,11 @@ static cudaError_t aggregate_launch_t(int B, int H, int W, int D, float gamma_d,
 
 size_t aggregate_tiled_smem(int D, int rho) { return agg_geom(D, rho).bytes; }
 
-__global__ void k_fill_i16(long long n, int16_t v, int16_t* __restrict__ p) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    p[i] = v;
-}
-
 cudaError_t launch_aggregate(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r,
                              const float* vol, const uint8_t* guide, const uint8_t* nan_map,
-                             float* out, int16_t* wta_k, cudaStream_t st) {
-  if (rho < 7)
-    return launch_aggregate_slide(B, H, W, D, rho, gamma_d, gamma_r, vol, guide, nan_map, out, wta_k,
-                                  st);
-  // rho = 7 (no registers left for the epilogue's WTA) and the tiled variant compute no
-  // WTA: every pixel says "scan the volume"
-  if (wta_k) {
-    const long long n = (long long)B * H * W;
-    k_fill_i16<<<(int)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, st>>>(n, (int16_t)-2, wta_k);
-    const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  if (rho == 7)
-    return launch_aggregate_slide(B, H, W, D, rho, gamma_d, gamma_r, vol, guide, nan_map, out, nullptr, st);
+                             float* out, cudaStream_t st) {
+  if (rho <= 7)
+    return launch_aggregate_slide(B, H, W, D, rho, gamma_d, gamma_r, vol, guide, nan_map, out, st);
 #define RSR_A(R) \
   case R: return aggregate_launch_t<R>(B, H, W, D, gamma_d, gamma_r, vol, guide, nan_map, out, st);
   switch (rho) {

@@ -112,7 +112,6 @@ struct SlideArgs {
   const uint8_t* guide;
   const uint8_t* nan_map;
   float* out;
-  int16_t* wta_k;        // optional: per-pixel WTA of the aggregated volume (k; -1 none; -2 not computed here)
 };
 
 // The CTA's segment.  The 1-D grid enumerates (strip rank, row chunk, frame x
@@ -374,10 +373,6 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
           mbar_arrive(&empty_w[stw]);
         }
         const int y = s.ya - 2 * RHO + i;
-        if (A.wta_k && y >= s.ya && x < A.W && l == 0 && pass == 0) {   // all-NaN pixels: no WTA
-          const size_t pix = s.pix0 + (size_t)y * A.W + x;
-          A.wta_k[pix] = -1;
-        }
         if (y >= s.ya && x < A.W) {
           float* o = A.out + (s.pix0 + (size_t)y * A.W + x) * A.D + s.k0 + koff;
 #pragma unroll
@@ -423,38 +418,14 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
         mbar_arrive(&empty_w[stw]);
       }
       const int y = s.ya - 2 * RHO + i;   // completing output row
-      // den == 0 exactly when the centre is skipped (all-NaN): 0 * inf = NaN
-      const float inv = CLEAN ? __frcp_rn(den) : 0.f;
-      const float r[8] = {fin[0].x * inv, fin[0].y * inv, fin[1].x * inv, fin[1].y * inv,
-                          fin[2].x * inv, fin[2].y * inv, fin[3].x * inv, fin[3].y * inv};
-      if (RHO < 7 && A.wta_k && y >= s.ya) {   // rho = 7: the host fills -2
-        // WTA of the completed row for rsr_disparity_maps (the values written below): the
-        // G lanes of a pixel hold its KS disparities.  Max over the group (NaN = missing),
-        // then the lowest k holding it -- k_disparity's "first strict maximum above -inf".
-        // The general path leaves -2 ("scan the volume").
-        const size_t pix = s.pix0 + (size_t)y * A.W + x;
-        if (CLEAN && g.nslab == 1 && (g.G & (g.G - 1)) == 0) {
-          float rv[8];
-#pragma unroll
-          for (int q = 0; q < 8; q++) rv[q] = koff + (q < 4 ? q : 4 * g.G + q - 4) < A.D ? r[q] : qnan();
-          float m = -INFINITY;
-#pragma unroll
-          for (int q = 0; q < 8; q++) m = fmaxf(m, rv[q]);
-          for (int o = g.G >> 1; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-          int kb = 0x7fff;
-#pragma unroll
-          for (int q = 7; q >= 0; q--)
-            if (rv[q] == m) kb = koff + (q < 4 ? q : 4 * g.G + q - 4);
-          for (int o = g.G >> 1; o >= 1; o >>= 1) kb = min(kb, __shfl_xor_sync(0xffffffffu, kb, o));
-          if (l == 0 && x < A.W) A.wta_k[pix] = (int16_t)(m > -INFINITY ? kb : -1);
-        } else if (l == 0 && x < A.W) {
-          A.wta_k[pix] = -2;
-        }
-      }
       if (y >= s.ya && x < A.W) {
         const size_t pix = s.pix0 + (size_t)y * A.W + x;
         float* o = A.out + pix * A.D + s.k0 + koff;
         if (CLEAN) {
+          // den == 0 exactly when the centre is skipped (all-NaN): 0 * inf = NaN
+          const float inv = __frcp_rn(den);
+          const float r[8] = {fin[0].x * inv, fin[0].y * inv, fin[1].x * inv, fin[1].y * inv,
+                              fin[2].x * inv, fin[2].y * inv, fin[3].x * inv, fin[3].y * inv};
 #pragma unroll
           for (int hh = 0; hh < 2; hh++) {
             const int kb = s.k0 + koff + 4 * g.G * hh;
@@ -593,7 +564,7 @@ static int sm_count() {
 template <int RHO>
 static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, float gamma_r,
                                   const float* vol, const uint8_t* guide, const uint8_t* nan_map,
-                                  float* out, int16_t* wta_k, cudaStream_t st) {
+                                  float* out, cudaStream_t st) {
   const SlideGeom g = slide_geom(D, RHO);
   auto kern = k_aggregate_slide<RHO>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.bytes);
@@ -623,7 +594,6 @@ static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, flo
   A.kd = -log2e / (gamma_d * gamma_d);
   A.kr = std::isinf(gamma_r) ? -1e-30f : -log2e / (gamma_r * gamma_r);
   A.vol = vol; A.guide = guide; A.nan_map = nan_map; A.out = out;
-  A.wta_k = wta_k;
   const long long nblk = cols * ((H + bestR - 1) / bestR);
   if (nblk > 0x7fffffffLL) return cudaErrorInvalidValue;
   kern<<<(unsigned)nblk, 32 * (g.G + SG_NPROD), g.bytes, st>>>(A);
@@ -634,9 +604,9 @@ size_t aggregate_slide_smem(int D, int rho, int H) { (void)H; return slide_geom(
 
 cudaError_t launch_aggregate_slide(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r,
                                    const float* vol, const uint8_t* guide, const uint8_t* nan_map,
-                                   float* out, int16_t* wta_k, cudaStream_t st) {
+                                   float* out, cudaStream_t st) {
 #define RSR_S(R) \
-  case R: return slide_launch_t<R>(B, H, W, D, gamma_d, gamma_r, vol, guide, nan_map, out, wta_k, st);
+  case R: return slide_launch_t<R>(B, H, W, D, gamma_d, gamma_r, vol, guide, nan_map, out, st);
   switch (rho) {
     RSR_S(0) RSR_S(1) RSR_S(2) RSR_S(3) RSR_S(4) RSR_S(5) RSR_S(6) RSR_S(7)
     default:

@@ -81,7 +81,7 @@ int rsr_cost_volume(rsr_shape s, rsr_cost_params p, const uint8_t* ref, const ui
 }
 
 int rsr_aggregate(rsr_shape s, int32_t D, rsr_agg_params p, const float* vol, const uint8_t* guide,
-                  const uint8_t* nan_map, float* out, int16_t* wta_k, void* stream) {
+                  const uint8_t* nan_map, float* out, void* stream) {
   if (!shape_ok(s) || !vol || !guide || !out) return RSR_E_ARG;
   if (D < 1 || D > 32767 || p.rho < 0 || p.rho > 10) return RSR_E_ARG;
   if (!(p.gamma_d > 0.f) || std::isinf(p.gamma_d) || !(p.gamma_r > 0.f)) return RSR_E_ARG;
@@ -90,7 +90,7 @@ int rsr_aggregate(rsr_shape s, int32_t D, rsr_agg_params p, const float* vol, co
   const long long nslab = (D + 63) / 64;
   if ((long long)s.batch * nslab > 65535) return RSR_E_ARG;
   return launched(rsr::launch_aggregate(s.batch, s.height, s.width, D, p.rho, p.gamma_d, p.gamma_r,
-                                        vol, guide, nan_map, out, wta_k, as_stream(stream)));
+                                        vol, guide, nan_map, out, as_stream(stream)));
 }
 
 int rsr_disparity(rsr_shape s, rsr_disp_params p, const float* agg_ref, const float* agg_tar,
@@ -130,19 +130,6 @@ int rsr_road_roll(rsr_shape s, int32_t u0, int32_t u1, int32_t v0, int32_t v1, c
   if (s.batch > 65535) return RSR_E_ARG;
   return launched(rsr::launch_road_roll(s.batch, s.height, s.width, u0, u1, v0, v1, disparity, out,
                                         as_stream(stream)));
-}
-
-int rsr_disparity_maps(rsr_shape s, rsr_disp_params p, const float* agg_ref, const float* agg_tar,
-                       const int16_t* wta_ref_k, const int16_t* wta_tar_k,
-                       const int32_t* shift, float* disparity, void* stream) {
-  if (!shape_ok(s) || !agg_ref || !agg_tar || !wta_ref_k || !wta_tar_k || !shift || !disparity)
-    return RSR_E_ARG;
-  if (p.d_hi < p.d_lo || (long long)p.d_hi - p.d_lo + 1 > 32767 || p.lrc_tol < 0) return RSR_E_ARG;
-  if (s.width > 32768 || s.height > 65535 || s.batch > 65535) return RSR_E_ARG;
-  const int D = p.d_hi - p.d_lo + 1;
-  return launched(rsr::launch_disparity_maps(s.batch, s.height, s.width, p.d_lo, D, p.lrc_tol, p.subpixel != 0,
-                                             agg_ref, agg_tar, wta_ref_k, wta_tar_k, shift,
-                                             disparity, as_stream(stream)));
 }
 
 int rsr_reconstruct(rsr_shape s, rsr_rig rig, const float* disparity, float* xyz, void* stream) {

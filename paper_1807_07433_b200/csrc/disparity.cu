@@ -144,78 +144,6 @@ __global__ void __launch_bounds__(256) k_disparity(int H, int W, int d_lo, int D
   }
 }
 
-// From the WTA maps of rsr_aggregate: k per pixel is read from the maps; a pixel
-// whose map says -2 (not computed by the aggregation: general path, tiled
-// variant) is scanned from its volume row exactly like k_disparity, so the
-// results are bitwise those of k_disparity.  Kept pixels read A[k-1..k+1] for
-// the parabola (12 bytes instead of the D-float row).  One thread per pixel.
-RSR_DEVINL int argmax_scan(const float* __restrict__ p, int D) {
-  float best = -INFINITY;
-  int kb = -1;
-  for (int k = 0; k < D; k++) {
-    const float v = __ldg(p + k);
-    if (v > best) { best = v; kb = k; }   // NaN never compares greater
-  }
-  return kb;
-}
-
-__global__ void __launch_bounds__(256) k_disparity_maps(int H, int W, int d_lo, int D, int tol, int subpix,
-                                                        const float* __restrict__ agg_ref,
-                                                        const float* __restrict__ agg_tar,
-                                                        const int16_t* __restrict__ kref,
-                                                        const int16_t* __restrict__ ktar,
-                                                        const int32_t* __restrict__ shift,
-                                                        float* __restrict__ disp) {
-  extern __shared__ int16_t krs[];  // [W]
-  const int v = blockIdx.x, b = blockIdx.y;
-  const size_t row = ((size_t)b * H + v) * W;
-  for (int u = threadIdx.x; u < W; u += blockDim.x) {
-    int k = ktar[row + u];
-    if (k == -2) k = argmax_scan(agg_tar + (row + u) * D, D);
-    krs[u] = (int16_t)k;
-  }
-  __syncthreads();
-  const float sv = (float)shift[(size_t)b * H + v];
-  for (int u = threadIdx.x; u < W; u += blockDim.x) {
-    int k = kref[row + u];
-    const float* p = agg_ref + (row + u) * D;
-    if (k == -2) k = argmax_scan(p, D);
-    float d = qnan();
-    if (k >= 0) {
-      const int up = u - (k + d_lo);
-      if (up >= 0 && up < W) {
-        const int kr = krs[up];
-        if (kr >= 0 && abs(k - kr) <= tol) {
-          float r = (float)(k + d_lo);
-          if (subpix && k >= 1 && k <= D - 2) {
-            // the three values around the winner: one or two sectors of this pixel's row
-            const float a = __ldg(p + k - 1), bb = __ldg(p + k), c = __ldg(p + k + 1);
-            const float den = 2.f * a + 2.f * c - 4.f * bb;
-            if (!(a != a) && !(c != c) && fabsf(den) > 1e-12f) r += __fdiv_rn(a - c, den);
-          }
-          d = r + sv;
-        }
-      }
-    }
-    disp[row + u] = d;
-  }
-}
-
-cudaError_t launch_disparity_maps(int B, int H, int W, int d_lo, int D, int tol, int subpix,
-                                  const float* agg_ref, const float* agg_tar, const int16_t* kref,
-                                  const int16_t* ktar, const int32_t* shift,
-                                  float* disp, cudaStream_t st) {
-  const size_t smem = sizeof(int16_t) * (size_t)W;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_disparity_maps, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  k_disparity_maps<<<dim3(H, B), 256, smem, st>>>(H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, kref,
-                                                  ktar, shift, disp);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_disparity(int B, int H, int W, int d_lo, int D, int tol, int subpix,
                              const float* agg_ref, const float* agg_tar, const int32_t* shift,
                              float* disp, int16_t* wta_ref, int16_t* wta_tar, cudaStream_t st) {

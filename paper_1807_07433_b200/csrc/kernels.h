@@ -29,13 +29,12 @@ cudaError_t launch_nan_maps(int B, int H, int W, int d_lo, int D, const float* i
 
 cudaError_t launch_aggregate(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r,
                              const float* vol, const uint8_t* guide, const uint8_t* nan_map,
-                             float* out, int16_t* wta_k, cudaStream_t st);
+                             float* out, cudaStream_t st);
 
 // sliding-window warp-specialised variant (rho <= 7); launch_aggregate dispatches to it
 cudaError_t launch_aggregate_slide(int B, int H, int W, int D, int rho, float gamma_d,
                                    float gamma_r, const float* vol, const uint8_t* guide,
-                                   const uint8_t* nan_map, float* out, int16_t* wta_k,
-                                   cudaStream_t st);
+                                   const uint8_t* nan_map, float* out, cudaStream_t st);
 size_t aggregate_slide_smem(int D, int rho, int H);
 size_t aggregate_tiled_smem(int D, int rho);
 
@@ -55,12 +54,5 @@ cudaError_t launch_road_model(int B, int H, int W, int su, int sv, int n_hyp, fl
 
 cudaError_t launch_road_roll(int B, int H, int W, int u0, int u1, int v0, int v1, const float* disp,
                              double* out, cudaStream_t st);
-
-// Steps 4-5 from the per-pixel WTA maps of rsr_aggregate (pixels with k = -2 are
-// scanned from the volumes); bitwise the same results as launch_disparity.
-cudaError_t launch_disparity_maps(int B, int H, int W, int d_lo, int D, int tol, int subpix,
-                                  const float* agg_ref, const float* agg_tar, const int16_t* kref,
-                                  const int16_t* ktar, const int32_t* shift,
-                                  float* disp, cudaStream_t st);
 
 }  // namespace rsr

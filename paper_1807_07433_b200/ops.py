@@ -89,9 +89,8 @@ def rsr_cost_volume(ref, warped, valid, rho_block, d_lo, d_hi, *, with_tar=True,
     return vol_ref, vol_tar, nan_ref, nan_tar
 
 
-def rsr_aggregate(vol, guide, rho, gamma_d, gamma_r, nan_map=None, out=None, wta_k=None):
-    """Step 3 (Eqs. 8-10): aggregated volume float32 [B,H,W,D].  Optional per-pixel WTA
-    map for rsr_disparity_maps: wta_k int16 [B,H,W] (-2 = not computed by this call)."""
+def rsr_aggregate(vol, guide, rho, gamma_d, gamma_r, nan_map=None, out=None):
+    """Step 3 (Eqs. 8-10): aggregated volume float32 [B,H,W,D]."""
     guide, s = _bhw(guide)
     B, H, W = guide.shape
     if vol.dim() == 3:
@@ -99,13 +98,11 @@ def rsr_aggregate(vol, guide, rho, gamma_d, gamma_r, nan_map=None, out=None, wta
     D = vol.shape[-1]
     _expect(vol, torch.float32, (B, H, W, D), "vol")
     out = torch.empty_like(vol) if out is None else out
-    if wta_k is not None:
-        _expect(wta_k, torch.int16, (B, H, W), "wta_k")
     if nan_map is not None:
         nan_map, _ = _bhw(nan_map)
     check("rsr_aggregate", lib().rsr_aggregate(
         s, D, RsrAggParams(rho, float(gamma_d), float(gamma_r)), _ptr(vol), _ptr(guide),
-        _ptr(nan_map), _ptr(out), _ptr(wta_k), _stream()))
+        _ptr(nan_map), _ptr(out), _stream()))
     return out
 
 
@@ -126,22 +123,6 @@ def rsr_disparity(agg_ref, agg_tar, shift, d_lo, d_hi, lrc_tol, subpixel=True, d
         RsrShape(B, H, W), RsrDispParams(d_lo, d_hi, lrc_tol, 1 if subpixel else 0), _ptr(agg_ref),
         _ptr(agg_tar), _ptr(shift), _ptr(disparity), _ptr(wta_ref), _ptr(wta_tar), _stream()))
     return disparity, wta_ref, wta_tar
-
-
-def rsr_disparity_maps(agg_ref, agg_tar, wta_ref_k, wta_tar_k, shift, d_lo, d_hi, lrc_tol,
-                       subpixel=True, disparity=None):
-    """Steps 4-5 from the aggregation's WTA maps (bitwise equal to rsr_disparity)."""
-    if agg_ref.dim() == 3:
-        agg_ref, agg_tar = agg_ref.unsqueeze(0), agg_tar.unsqueeze(0)
-    B, H, W, D = agg_ref.shape
-    shift = shift.reshape(B, H)
-    _expect(wta_ref_k, torch.int16, (B, H, W), "wta_ref_k")
-    _expect(wta_tar_k, torch.int16, (B, H, W), "wta_tar_k")
-    disparity = torch.empty((B, H, W), dtype=torch.float32, device=agg_ref.device) if disparity is None else disparity
-    check("rsr_disparity_maps", lib().rsr_disparity_maps(
-        RsrShape(B, H, W), RsrDispParams(d_lo, d_hi, lrc_tol, 1 if subpixel else 0), _ptr(agg_ref), _ptr(agg_tar),
-        _ptr(wta_ref_k), _ptr(wta_tar_k), _ptr(shift), _ptr(disparity), _stream()))
-    return disparity
 
 
 def rsr_reconstruct(disparity, f, baseline, u0=None, v0=None, d_min=1.0, xyz=None):

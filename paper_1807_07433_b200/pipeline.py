@@ -37,9 +37,9 @@ class StereoParams:
 class StereoPipeline:
     """Pre-allocated buffers for a [B,H,W] batch; run() enqueues the whole path.
 
-    Kernel launches per run(with_wta=False): warp 1; cost volume 2 block-stats +
-    2 x ceil(D/64) NCC slabs + 1 NaN-summary; aggregation 2 (rho <= 7);
-    disparity from the WTA maps 1; reconstruction 1 (see launches()).
+    Kernel launches per run(): warp 1; cost volume 2 block-stats + 2 x ceil(D/64)
+    NCC slabs + 1 NaN-summary; aggregation 2 (rho <= 7); disparity 1;
+    reconstruction 1 (see launches()).
     """
 
     @staticmethod
@@ -65,9 +65,6 @@ class StereoPipeline:
         self.wta_tar = e((B, H, W), torch.int16)
         self.xyz = e((B, H, W, 3), torch.float32)
         self.workspace = e((ops.cost_workspace_bytes(B, H, W),), torch.uint8)
-        # per-pixel winner-take-all maps written by the aggregations (rsr_disparity_maps)
-        self.wk_ref = e((B, H, W), torch.int16)
-        self.wk_tar = e((B, H, W), torch.int16)
         self._side = None
 
     def run(self, left, right, alpha_beta, with_wta=True):
@@ -86,18 +83,13 @@ class StereoPipeline:
         self._side.wait_event(fork)
         with torch.cuda.stream(self._side):
             ops.rsr_aggregate(self.vol_tar, self.warped, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_tar,
-                              self.agg_tar, wta_k=self.wk_tar)
-        ops.rsr_aggregate(self.vol_ref, left, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_ref, self.agg_ref,
-                          wta_k=self.wk_ref)
+                              self.agg_tar)
+        ops.rsr_aggregate(self.vol_ref, left, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_ref, self.agg_ref)
         join = torch.cuda.Event()
         join.record(self._side)
         main.wait_event(join)
-        # steps 4-5 from the aggregations' WTA maps (bitwise equal to rsr_disparity, which
-        # re-reads both volumes); with_wta also fills the full k maps via rsr_disparity
-        ops.rsr_disparity_maps(self.agg_ref, self.agg_tar, self.wk_ref, self.wk_tar, self.shift,
-                               p.d_lo, p.d_hi, p.lrc_tol, p.subpixel, self.disparity)
-        if with_wta:
-            ops.rsr_disparity(self.agg_ref, self.agg_tar, self.shift, p.d_lo, p.d_hi, p.lrc_tol, p.subpixel,
-                              torch.empty_like(self.disparity), self.wta_ref, self.wta_tar)
+        ops.rsr_disparity(self.agg_ref, self.agg_tar, self.shift, p.d_lo, p.d_hi, p.lrc_tol, p.subpixel,
+                          self.disparity, self.wta_ref if with_wta else None,
+                          self.wta_tar if with_wta else None)
         ops.rsr_reconstruct(self.disparity, p.focal, p.baseline, d_min=p.d_min, xyz=self.xyz)
         return self.disparity

@@ -52,14 +52,11 @@ def test_validation_without_gpu(L):
     assert L.rsr_cost_volume(s, RsrCostParams(5, 0, 3), fake, fake, fake, fake, None, None, None,
                              fake, ws, None) == 3   # 8 < 2*5+1
     assert L.rsr_aggregate(s, 0, RsrAggParams(1, 1.0, 1.0), fake, fake, None, ctypes.c_void_p(32),
-                           None, None) == 2
+                           None) == 2
     assert L.rsr_aggregate(s, 4, RsrAggParams(11, 1.0, 1.0), fake, fake, None, ctypes.c_void_p(32),
-                           None, None) == 2
+                           None) == 2
     assert L.rsr_aggregate(s, 4, RsrAggParams(1, 1.0, float("nan")), fake, fake, None,
-                           ctypes.c_void_p(32), None, None) == 2
-    # WTA maps are required by rsr_disparity_maps
-    assert L.rsr_disparity_maps(s, RsrDispParams(0, 3, 1, 1), fake, fake, None, fake, fake, fake, None) == 2
-    assert L.rsr_disparity_maps(s, RsrDispParams(0, 3, 1, 1), fake, fake, fake, None, fake, fake, None) == 2
+                           ctypes.c_void_p(32), None) == 2
     assert L.rsr_disparity(s, RsrDispParams(0, 3, -1, 1), fake, fake, fake, fake, None, None, None) == 2
     assert L.rsr_reconstruct(s, RsrRig(0.0, 0.12, 0, 0, 1.0), fake, fake, None) == 2
     assert L.rsr_reconstruct(s, RsrRig(700.0, 0.12, 0, 0, 0.0), fake, fake, None) == 2

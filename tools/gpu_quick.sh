@@ -3,7 +3,7 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 TAG=${TAG:-q}
-timeout ${PYT_TIMEOUT:-900} python -m pytest tests -m gpu -x -q ${PYTEST_ARGS} > gpurun_out/${TAG}_pytest_gpu.log 2>&1; rc=$?
+timeout ${PYT_TIMEOUT:-900} python -m pytest tests -m gpu -x -q ${PYTEST_ARGS} ${PYK:+-k "$PYK"} > gpurun_out/${TAG}_pytest_gpu.log 2>&1; rc=$?
 echo "pytest rc=$rc" >> gpurun_out/${TAG}_pytest_gpu.log; tail -30 gpurun_out/${TAG}_pytest_gpu.log
 [ $rc -ne 0 ] && [ -z "$BENCH_ANYWAY" ] && exit 1
 timeout 600 python bench.py ${BENCH_ARGS} > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?"
