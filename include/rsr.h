@@ -221,6 +221,48 @@ int rsr_road_model(rsr_shape s, rsr_road_params p, const float* disparity, doubl
 int rsr_road_roll(rsr_shape s, int32_t u0, int32_t u1, int32_t v0, int32_t v1,
                   const float* disparity, double* out, void* stream);
 
+/* ------------------------------------------------------------------------ */
+/* Restricted search range (P:251 future work: "reduce the search range and */
+/* only perform the bilateral filtering on the space around the calculated   */
+/* disparities"; reading 20).  From the previous frame's total     */
+/* disparities d (rsr_disparity) and the next frame's row shifts s          */
+/* (rsr_warp): range[b] = {floor(min r) - delta, ceil(max r) + delta} over the */
+/* finite entries of r = d - s(v) (fp64), clipped to [d_lo_limit,            */
+/* d_hi_limit]; the limits when frame b's map has no finite entry.  The next */
+/* frame's path then runs with d_lo, d_hi = that range (a smaller D).        */
+/*   disparity : float [B][H][W];  shift : int32 [B][H];                      */
+/*   range     : int32 [B][2] out (d_lo, d_hi per frame; a batch takes the   */
+/*               union)                                                       */
+/* Errors: RSR_E_ARG on NULL pointers, delta < 0, d_hi_limit < d_lo_limit or */
+/* a limit span above 32767.                                                  */
+int rsr_search_range(rsr_shape s, const float* disparity, const int32_t* shift, int32_t delta,
+                     int32_t d_lo_limit, int32_t d_hi_limit, int32_t* range, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Reconstruction accuracy: "the four corners s_1..s_4 are       */
+/* interpolated into a ground plane n0 x + n1 y + n2 z + n3 = 0 ... then we  */
+/* estimate the distances between [points on the model] and the road        */
+/* surface" (reading 19).                                          */
+/* rsr_plane_fit: total-least-squares plane of each frame's n_corners >= 3   */
+/* corners: unit normal = eigenvector of the centred corners' scatter matrix */
+/* with the smallest eigenvalue (fp64 Jacobi), n3 = -n . centroid, oriented */
+/* n3 > 0 (camera side positive; n3 == 0: last non-zero normal entry > 0).  */
+/*   corners : double [batch][n_corners][3] (x, y, z, metres, as rsr_reconstruct) */
+/*   plane   : double [batch][4] out; NaN if a corner is not finite or the   */
+/*             corners span no plane (sigma_2 <= 1e-12 sigma_1)               */
+/* Errors: RSR_E_ARG on NULL pointers, batch < 1 or n_corners < 3.           */
+int rsr_plane_fit(int32_t batch, int32_t n_corners, const double* corners, double* plane,
+                  void* stream);
+
+/* rsr_plane_distance: signed distance n . p + n3 of every reconstructed      */
+/* point to its frame's plane (fp64, stored as float; positive on the camera  */
+/* side, i.e. height above the road; NaN for NaN points).                     */
+/*   plane : double [B][4] (rsr_plane_fit);  xyz : float [B][H][W][3];        */
+/*   dist  : float [B][H][W] out                                              */
+/* Errors: RSR_E_ARG on NULL pointers.                                        */
+int rsr_plane_distance(rsr_shape s, const double* plane, const float* xyz, float* dist,
+                       void* stream);
+
 /* Human-readable text for a status code (static storage). */
 const char* rsr_strerror(int status);
 

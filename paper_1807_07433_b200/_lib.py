@@ -72,6 +72,12 @@ def lib() -> ctypes.CDLL:
         L.rsr_road_roll.argtypes = [RsrShape, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                     P, P, P]
         L.rsr_road_roll.restype = ctypes.c_int
+        L.rsr_search_range.argtypes = [RsrShape, P, P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P]
+        L.rsr_search_range.restype = ctypes.c_int
+        L.rsr_plane_fit.argtypes = [ctypes.c_int32, ctypes.c_int32, P, P, P]
+        L.rsr_plane_fit.restype = ctypes.c_int
+        L.rsr_plane_distance.argtypes = [RsrShape, P, P, P, P]
+        L.rsr_plane_distance.restype = ctypes.c_int
         L.rsr_strerror.argtypes = [ctypes.c_int]
         L.rsr_strerror.restype = ctypes.c_char_p
         L.rsr_version.restype = ctypes.c_int

@@ -132,6 +132,25 @@ int rsr_road_roll(rsr_shape s, int32_t u0, int32_t u1, int32_t v0, int32_t v1, c
                                         as_stream(stream)));
 }
 
+int rsr_search_range(rsr_shape s, const float* disparity, const int32_t* shift, int32_t delta,
+                     int32_t d_lo_limit, int32_t d_hi_limit, int32_t* range, void* stream) {
+  if (!shape_ok(s) || !disparity || !shift || !range) return RSR_E_ARG;
+  if (delta < 0 || d_hi_limit < d_lo_limit || (long long)d_hi_limit - d_lo_limit + 1 > 32767) return RSR_E_ARG;
+  if (s.batch > 0x7fffffff / 2) return RSR_E_ARG;
+  return launched(rsr::launch_search_range(s.batch, s.height, s.width, delta, d_lo_limit, d_hi_limit, disparity,
+                                           shift, range, as_stream(stream)));
+}
+
+int rsr_plane_fit(int32_t batch, int32_t n_corners, const double* corners, double* plane, void* stream) {
+  if (!corners || !plane || batch < 1 || n_corners < 3) return RSR_E_ARG;
+  return launched(rsr::launch_plane_fit(batch, n_corners, corners, plane, as_stream(stream)));
+}
+
+int rsr_plane_distance(rsr_shape s, const double* plane, const float* xyz, float* dist, void* stream) {
+  if (!shape_ok(s) || !plane || !xyz || !dist) return RSR_E_ARG;
+  return launched(rsr::launch_plane_distance(s.batch, s.height, s.width, plane, xyz, dist, as_stream(stream)));
+}
+
 int rsr_reconstruct(rsr_shape s, rsr_rig rig, const float* disparity, float* xyz, void* stream) {
   if (!shape_ok(s) || !disparity || !xyz) return RSR_E_ARG;
   if (!(rig.f > 0) || !(rig.baseline > 0) || !(rig.d_min > 0)) return RSR_E_ARG;

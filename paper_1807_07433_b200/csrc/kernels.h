@@ -55,4 +55,13 @@ cudaError_t launch_road_model(int B, int H, int W, int su, int sv, int n_hyp, fl
 cudaError_t launch_road_roll(int B, int H, int W, int u0, int u1, int v0, int v1, const float* disp,
                              double* out, cudaStream_t st);
 
+// reconstruction accuracy (plane.cu)
+cudaError_t launch_plane_fit(int B, int K, const double* corners, double* plane, cudaStream_t st);
+cudaError_t launch_plane_distance(int B, int H, int W, const double* plane, const float* xyz, float* dist,
+                                  cudaStream_t st);
+
+// restricted search range (range.cu)
+cudaError_t launch_search_range(int B, int H, int W, int delta, int lo_lim, int hi_lim, const float* disp,
+                                const int32_t* shift, int32_t* range, cudaStream_t st);
+
 }  // namespace rsr

@@ -172,3 +172,47 @@ def rsr_road_roll(disparity, u0, u1, v0, v1, out=None):
 
 
 _ = math  # (kept for callers that pass math.inf for gamma_r)
+
+
+def rsr_plane_fit(corners, plane=None):
+    """Accuracy evaluation: total-least-squares ground plane of each frame's
+    corners, float64 [B,K,3] (K >= 3) -> float64 [B,4] = (n0, n1, n2, n3), NaN if degenerate."""
+    if corners.dim() == 2:
+        corners = corners.unsqueeze(0)
+    B, K, _ = corners.shape
+    _expect(corners, torch.float64, (B, K, 3), "corners")
+    plane = torch.empty((B, 4), dtype=torch.float64, device=corners.device) if plane is None else plane
+    _expect(plane, torch.float64, (B, 4), "plane")
+    check("rsr_plane_fit", lib().rsr_plane_fit(B, K, _ptr(corners), _ptr(plane), _stream()))
+    return plane
+
+
+def rsr_plane_distance(plane, xyz, dist=None):
+    """Signed distance of every reconstructed point (float32 [B,H,W,3]) to its frame's
+    plane (float64 [B,4]): float32 [B,H,W], positive on the camera side."""
+    if xyz.dim() == 3:
+        xyz = xyz.unsqueeze(0)
+    B, H, W, _ = xyz.shape
+    plane = plane.reshape(-1, 4)
+    _expect(xyz, torch.float32, (B, H, W, 3), "xyz")
+    _expect(plane, torch.float64, (B, 4), "plane")
+    dist = torch.empty((B, H, W), dtype=torch.float32, device=xyz.device) if dist is None else dist
+    check("rsr_plane_distance", lib().rsr_plane_distance(RsrShape(B, H, W), _ptr(plane), _ptr(xyz), _ptr(dist),
+                                                         _stream()))
+    return dist
+
+
+def rsr_search_range(disparity, shift, delta, d_lo_limit, d_hi_limit, out=None):
+    """Restricted search range: per-frame residual band [d_lo, d_hi] of the
+    previous frame's disparities (float32 [B,H,W]) around the next frame's shifts
+    (int32 [B,H]); int32 [B,2]."""
+    if disparity.dim() == 2:
+        disparity = disparity.unsqueeze(0)
+    B, H, W = disparity.shape
+    _expect(disparity, torch.float32, (B, H, W), "disparity")
+    shift = shift.reshape(B, H)
+    _expect(shift, torch.int32, (B, H), "shift")
+    out = torch.empty((B, 2), dtype=torch.int32, device=disparity.device) if out is None else out
+    check("rsr_search_range", lib().rsr_search_range(RsrShape(B, H, W), _ptr(disparity), _ptr(shift), int(delta),
+                                                     int(d_lo_limit), int(d_hi_limit), _ptr(out), _stream()))
+    return out
