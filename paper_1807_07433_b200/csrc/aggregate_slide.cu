@@ -52,22 +52,30 @@ constexpr short SG_GSKIP = 600;     // integer guide tile: skipped pixel (outsid
 constexpr int SG_RLUT = 2 * 600 + 255 + 1;   // range table, zero beyond |dg| = 255
 
 struct SlideGeom {
-  int G, KS, nslab, CX, XS, WST, GR;
+  int G, KS, CS, nslab, CX, XS, WST, GR;
   size_t off_cost, off_w, off_dpart, off_guide, off_rlut, off_bar, bytes;
 };
 
 // KS = disparities per slab (multiple of 8, <= 64), G = consumer lanes per column
-__host__ __device__ inline SlideGeom slide_geom(int D, int rho) {
+// rows = output rows the guide tile must hold (SG_SEGMAX for the one-CTA-per-SM
+// kernels; the launch's R for the two-CTA variants, which need the space)
+__host__ __device__ inline SlideGeom slide_geom(int D, int rho, int rows = SG_SEGMAX, bool compact = false) {
   SlideGeom g;
   const int NT = 2 * rho + 1;
   g.nslab = (D + 63) / 64;
   const int per = (D + g.nslab - 1) / g.nslab;
   g.KS = (per + 7) & ~7;
   g.G = g.KS / 8;
+  // cost column stride in the stage ring.  compact (the two-CTA small-slab kernels):
+  // D itself when one slab holds all of D and rows stay 16-byte aligned, so a whole
+  // row segment is one contiguous bulk copy (the lanes past D then read the next
+  // column's costs: finite or NaN garbage in k slots that are never stored).  Else
+  // KS with a filled tail.
+  g.CS = (compact && g.nslab == 1 && (D & 3) == 0) ? D : g.KS;
   g.CX = 32 + 2 * rho;
   g.XS = 16 * NT + 4;                 // == 20 (mod 32): 4 / 8 columns hit distinct banks
   g.WST = 32 * g.XS + 32;             // weights [x][tap][age16] + completing rows' weight sums
-  g.GR = SG_SEGMAX + 4 * rho;
+  g.GR = rows + 4 * rho;
   size_t o = 0;
   g.off_cost = o;  o += sizeof(float) * (size_t)SG_NSC * g.CX * g.KS;
   g.off_w = o;     o += sizeof(float) * (size_t)SG_NSW * g.WST;
@@ -166,23 +174,23 @@ __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g
                       gt[(i + RHO) * g.CX + col] == SG_GSKIP;
     cp[h] = !skip && bulk;
     if (col < g.CX) {
-      float* d = dst + col * g.KS;
+      float* d = dst + col * g.CS;
       if (!skip && !bulk) {
         const float* sp = A.vol + (rowpix + xx) * A.D + s.k0;
-        for (int k = 0; k < g.KS; k++) d[k] = k < s.ks_eff ? sp[k] : fillv;
+        for (int k = 0; k < g.CS; k++) d[k] = k < s.ks_eff ? sp[k] : fillv;
       } else if (skip) {
-        for (int k = 0; k < g.KS; k += 4) *reinterpret_cast<float4*>(d + k) = make_float4(fillv, fillv, fillv, fillv);
-      } else if (s.ks_eff < g.KS) {
-        for (int k = s.ks_eff; k < g.KS; k++) d[k] = fillv;   // slab tail (the copy fills the head)
+        for (int k = 0; k < g.CS; k += 4) *reinterpret_cast<float4*>(d + k) = make_float4(fillv, fillv, fillv, fillv);
+      } else if (s.ks_eff < g.CS) {
+        for (int k = s.ks_eff; k < g.CS; k++) d[k] = fillv;   // slab tail (the copy fills the head)
       }
     }
   }
   const uint32_t ncols = __popc(__ballot_sync(0xffffffffu, cp[0])) + __popc(__ballot_sync(0xffffffffu, cp[1]));
   __syncwarp();
   const float* src = A.vol + (rowpix + (s.x0 - RHO)) * A.D + s.k0;
-  if (ncols == (uint32_t)g.CX && g.KS == A.D) {
+  if (ncols == (uint32_t)g.CX && g.CS == A.D) {
     // whole row segment in the image and one contiguous run: a single bulk copy
-    const uint32_t bytes = (uint32_t)g.CX * g.KS * 4u;
+    const uint32_t bytes = (uint32_t)g.CX * g.CS * 4u;
     if (lane == 0) {
       mbar_arrive_expect_tx(&full_c[st], bytes);
       bulk_g2s(dst, src, bytes, &full_c[st]);
@@ -194,7 +202,7 @@ __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       const int col = lane + 32 * h;
-      if (cp[h]) bulk_g2s(dst + col * g.KS, src + (size_t)col * A.D, bytes_col, &full_c[st]);
+      if (cp[h]) bulk_g2s(dst + col * g.CS, src + (size_t)col * A.D, bytes_col, &full_c[st]);
     }
   }
 }
@@ -288,19 +296,19 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
 // valid or skipped, NQ = 2).
 template <int RHO, int MODE>
 RSR_DEVINL void slide_row(float2 (&acc)[2 * RHO + 1][4], float2 (&fin)[4], const float* crow,
-                          const float* wrow, int KS, int G) {
+                          const float* wrow, int CS, int G) {
   constexpr int NT = 2 * RHO + 1;
   constexpr int NQ = MODE == 2 ? 2 : 4;
 #pragma unroll
   for (int j = 0; j < NT; j++) {
     float2 cp[4];
     if (MODE == 0) {
-      const float4 ca = *reinterpret_cast<const float4*>(crow + j * KS);
-      const float4 cb = *reinterpret_cast<const float4*>(crow + j * KS + 4 * G);
+      const float4 ca = *reinterpret_cast<const float4*>(crow + j * CS);
+      const float4 cb = *reinterpret_cast<const float4*>(crow + j * CS + 4 * G);
       cp[0] = make_float2(ca.x, ca.y); cp[1] = make_float2(ca.z, ca.w);
       cp[2] = make_float2(cb.x, cb.y); cp[3] = make_float2(cb.z, cb.w);
     } else {
-      const float4 t = *reinterpret_cast<const float4*>(crow + j * KS);
+      const float4 t = *reinterpret_cast<const float4*>(crow + j * CS);
       const float tv[4] = {t.x, t.y, t.z, t.w};
       if (MODE == 1) {
 #pragma unroll
@@ -402,15 +410,15 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
       const int stc = it % SG_NSC, stw = it % SG_NSW;
       mbar_wait_parity(&full_c[stc], (it / SG_NSC) & 1);
       mbar_wait_parity(&full_w[stw], (it / SG_NSW) & 1);
-      const float* crow = cost_s + (size_t)stc * g.CX * g.KS + xl * g.KS + koff;
+      const float* crow = cost_s + (size_t)stc * g.CX * g.KS + xl * g.CS + koff;
       const float* wrow = w_s + (size_t)stw * g.WST + xl * g.XS;
       float2 fin[4];
       if (CLEAN)
-        slide_row<RHO, 0>(acc, fin, crow, wrow, g.KS, g.G);
+        slide_row<RHO, 0>(acc, fin, crow, wrow, g.CS, g.G);
       else if (hc)
-        slide_row<RHO, 2>(acc, fin, crow, wrow, g.KS, g.G);
+        slide_row<RHO, 2>(acc, fin, crow, wrow, g.CS, g.G);
       else
-        slide_row<RHO, 1>(acc, fin, crow, wrow, g.KS, g.G);
+        slide_row<RHO, 1>(acc, fin, crow, wrow, g.CS, g.G);
       const float den = (CLEAN || hc) ? wrow[(32 - xl) * g.XS + xl] : 0.f;
       __syncwarp();
       if (lane == 0) {
@@ -462,10 +470,14 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
   }
 }
 
-template <int RHO>
-__global__ void __launch_bounds__(384, 1) k_aggregate_slide(const SlideArgs A) {
+// MINB = 1: up to 8 consumer warps (D up to 64 per slab), one CTA per SM.  MINB = 2:
+// small slabs (G <= 2 at any rho, G <= 4 at rho <= 5), two CTAs per SM so the few
+// consumer warps of a CTA do not leave the SM idle; the guide tile is sized by R.
+template <int RHO, int MINB, bool COMPACT>
+__global__ void __launch_bounds__(MINB == 1 ? 384 : (RHO <= 5 ? 256 : 192), MINB)
+    k_aggregate_slide(const SlideArgs A) {
   extern __shared__ __align__(128) unsigned char sl_smem[];
-  const SlideGeom g = slide_geom(A.D, RHO);
+  const SlideGeom g = slide_geom(A.D, RHO, MINB == 1 ? SG_SEGMAX : A.R, COMPACT);
   float* cost_s = reinterpret_cast<float*>(sl_smem + g.off_cost);
   float* w_s = reinterpret_cast<float*>(sl_smem + g.off_w);
   float* dpart = reinterpret_cast<float*>(sl_smem + g.off_dpart);
@@ -565,29 +577,33 @@ template <int RHO>
 static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, float gamma_r,
                                   const float* vol, const uint8_t* guide, const uint8_t* nan_map,
                                   float* out, cudaStream_t st) {
-  const SlideGeom g = slide_geom(D, RHO);
-  auto kern = k_aggregate_slide<RHO>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.bytes);
-  if (e != cudaSuccess) { cudaGetLastError(); return e; }
+  const SlideGeom g1 = slide_geom(D, RHO);
   SlideArgs A;
   A.B = B; A.H = H; A.W = W; A.D = D;
   const int nstrips = (W + 31) / 32;
-  const long long cols = (long long)nstrips * B * g.nslab;
-  // rows per CTA: minimise (waves of one-CTA-per-SM launches) x (rows + 2 rho warm-up)
+  const long long cols = (long long)nstrips * B * g1.nslab;
   const int nsm = sm_count();
-  int bestR = min(H, SG_SEGMAX);
+  // two CTAs per SM for small slabs (few consumer warps), if the guide tile of R rows
+  // leaves room for two: at most 113 KB each
+  const bool small = g1.G <= (RHO <= 5 ? 4 : 2);
+  const int minb = small ? 2 : 1;
+  auto fits = [&](int R) { return minb == 1 || slide_geom(D, RHO, R).bytes <= 113 * 1024; };
+  // rows per CTA: minimise (waves of minb-CTAs-per-SM launches) x (rows + 2 rho warm-up)
+  int bestR = 0;
   double best = 1e300;
   for (int n = (H + SG_SEGMAX - 1) / SG_SEGMAX; n <= H; n++) {
     const int R = (H + n - 1) / n;
     if (R < 8 && n > 1) break;
+    if (!fits(R)) continue;
     const long long ctas = cols * ((H + R - 1) / R);
-    const double cost = (double)((ctas + nsm - 1) / nsm) * (R + 2 * RHO);
+    const double cost = (double)((ctas + (long long)minb * nsm - 1) / ((long long)minb * nsm)) * (R + 2 * RHO);
     if (cost < best * 0.999) { best = cost; bestR = R; }
   }
   if (const char* e = getenv("RSR_K3_ROWS")) {   // experiment hook (tools/): force R
     const int r = atoi(e);
-    if (r >= 8 && r <= SG_SEGMAX) bestR = r;
+    if (r >= 8 && r <= SG_SEGMAX && fits(r)) bestR = r;
   }
+  if (bestR == 0) bestR = 8;
   A.R = bestR;
   A.nstrips = nstrips;
   const float log2e = 1.4426950408889634f;
@@ -596,7 +612,15 @@ static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, flo
   A.vol = vol; A.guide = guide; A.nan_map = nan_map; A.out = out;
   const long long nblk = cols * ((H + bestR - 1) / bestR);
   if (nblk > 0x7fffffffLL) return cudaErrorInvalidValue;
-  kern<<<(unsigned)nblk, 32 * (g.G + SG_NPROD), g.bytes, st>>>(A);
+  const size_t bytes = minb == 1 ? g1.bytes : slide_geom(D, RHO, bestR).bytes;
+  // compact cost rows (one bulk copy per row) where D < KS and rows stay aligned; the
+  // compact kernels spill a little more, so D == KS keeps the padded layout
+  const bool compact = small && g1.nslab == 1 && (D & 3) == 0 && D < g1.KS;
+  auto kern = minb == 1 ? k_aggregate_slide<RHO, 1, false>
+                        : (compact ? k_aggregate_slide<RHO, 2, true> : k_aggregate_slide<RHO, 2, false>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) { cudaGetLastError(); return e; }
+  kern<<<(unsigned)nblk, 32 * (g1.G + SG_NPROD), bytes, st>>>(A);
   return cudaGetLastError();
 }
 

@@ -225,6 +225,11 @@ EDGE_CASES = {
     "D200_two_slabs": (20, 48, -100, 99, 1, 1, 2.0, 10.0, 0.0, 0.0),
     "rho7_D96": (40, 130, -48, 47, 4, 7, 5.0, 12.0, 0.1, 5.0),
     "D48": (33, 97, -24, 23, 3, 5, 4.0, 10.0, 0.08, 4.0),
+    # two-CTA small-slab kernels: the paper's D = 30 (rows not 16-byte aligned:
+    # copy spread over the producers) and D = 28 (compact rows, one bulk copy)
+    "D30_rho4": (41, 133, -15, 14, 3, 4, 4.0, 12.0, 0.05, 3.0),
+    "D28_rho4": (35, 101, -14, 13, 2, 4, 4.0, 12.0, 0.05, 3.0),
+    "D12_rho6": (44, 90, -6, 5, 2, 6, 4.0, 12.0, 0.1, 2.0),
 }
 
 
