@@ -150,10 +150,18 @@ RSR_DEVINL Seg cta_segment(const SlideArgs& A, const SlideGeom& g) {
 // or one for the whole row segment when it is contiguous; skipped columns
 // (outside the image, or all-NaN on a clean segment) are filled with 0 (clean)
 // or NaN (general path).
+// rows of an even D that is not a multiple of 4 (no 16-byte bulk copies) with a
+// power-of-two KS: staged by 8-byte cp.async spread over all producer threads,
+// coalesced along k; the full barrier then expects 33 arrivals per producer warp
+// (each lane's cp.async arrive, and lane 0 after the warp's fills)
+__host__ __device__ inline bool stage_cpasync(int D, const SlideGeom& g) {
+  return (D & 3) == 2 && (g.KS & (g.KS - 1)) == 0;
+}
+
 template <int RHO>
 __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g, const Seg& s, bool clean,
                                           int i, const short* gt, float* cost_s, uint64_t* full_c, uint64_t* empty_c,
-                                          uint32_t& it_c, int lane) {
+                                          uint32_t& it_c, int lane, int t = 0, int nt = 32) {
   const bool bulk = (A.D & 3) == 0;
   const float fillv = clean ? 0.f : qnan();
   const int st = it_c % SG_NSC;
@@ -163,6 +171,25 @@ __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g
   float* dst = cost_s + (size_t)st * g.CX * g.KS;
   const bool row_in = yy >= 0 && yy < A.H;
   const size_t rowpix = s.pix0 + (size_t)yy * A.W;
+  if (stage_cpasync(A.D, g)) {
+    const int lg = __ffs(g.KS) - 2;   // log2(KS / 2): float pairs per column
+    for (int e = t; e < (g.CX << lg); e += nt) {
+      const int col = e >> lg, k = 2 * (e & ((1 << lg) - 1));
+      float* d = dst + col * g.KS + k;
+      // the guide tile marks outside and all-NaN pixels: filled, not copied
+      const bool skip = !row_in || gt[(i + RHO) * g.CX + col] == SG_GSKIP;
+      if (!skip && k < s.ks_eff) {
+        cp_async8(d, A.vol + (rowpix + (s.x0 - RHO + col)) * A.D + s.k0 + k);
+      } else {
+        d[0] = fillv;
+        d[1] = fillv;
+      }
+    }
+    cp_async_mbar_arrive_noinc(&full_c[st]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&full_c[st]);   // this warp's fills are in
+    return;
+  }
   bool cp[2];
 #pragma unroll
   for (int h = 0; h < 2; h++) {
@@ -236,11 +263,14 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
     for (int j = 0; j < NT; j++)
       sreg[n][j] = ex2_ftz((float)((j - RHO) * (j - RHO) + (RHO - a) * (RHO - a)) * A.kd);
   }
+  const bool cpa = stage_cpasync(A.D, g);
   for (int pass = 0; pass < npass; pass++) {
     for (int e = p * 32 + lane; e < NT * 32; e += SG_NPROD * 32) dsum[e] = 0.f;
     asm volatile("bar.sync 1, %0;" ::"r"(SG_NPROD * 32) : "memory");
     for (int i = 0; i < NR; i++, it_w++) {
-      if (p == 0) stage_row<RHO>(A, g, s, clean, i, gt, cost_s, full_c, empty_c, it_c, lane);
+      // cp.async-staged rows: every producer warp issues a share (non-blocking)
+      if (cpa || p == 0)
+        stage_row<RHO>(A, g, s, clean, i, gt, cost_s, full_c, empty_c, it_c, lane, p * 32 + lane, SG_NPROD * 32);
       const int st = it_w % SG_NSW;
       if (it_w >= SG_NSW) mbar_wait_parity(&empty_w[st], ((it_w / SG_NSW) & 1) ^ 1);
       float* wst = w_s + (size_t)st * g.WST;
@@ -497,7 +527,8 @@ __global__ void __launch_bounds__(MINB == 1 ? 384 : (RHO <= 5 ? 256 : 192), MINB
   const int n_cons = g.G;   // consumer warps
   if (tid == 0) {
     for (int q = 0; q < SG_NSC; q++) {
-      mbar_init(&full_c[q], 1);
+      // cp.async-staged rows: each producer thread's cp.async arrive + one per warp after its fills
+      mbar_init(&full_c[q], stage_cpasync(A.D, g) ? SG_NPROD * 33 : 1);
       mbar_init(&empty_c[q], n_cons);
     }
     for (int q = 0; q < SG_NSW; q++) {

@@ -84,6 +84,18 @@ RSR_DEVINL float clamp_unit_keep_nan(float c) {
 RSR_DEVINL uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+
+// 8-byte asynchronous global -> shared copy (cp.async, LDGSTS); completion tracked
+// by an mbarrier through cp_async_mbar_arrive_noinc
+RSR_DEVINL void cp_async8(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+
+// arrive on bar once every cp.async this thread issued so far has landed (counts as
+// one of the barrier's expected arrivals)
+RSR_DEVINL void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 RSR_DEVINL void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }

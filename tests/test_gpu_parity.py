@@ -230,6 +230,9 @@ EDGE_CASES = {
     "D30_rho4": (41, 133, -15, 14, 3, 4, 4.0, 12.0, 0.05, 3.0),
     "D28_rho4": (35, 101, -14, 13, 2, 4, 4.0, 12.0, 0.05, 3.0),
     "D12_rho6": (44, 90, -6, 5, 2, 6, 4.0, 12.0, 0.1, 2.0),
+    # D % 4 == 2 rows staged by 8-byte cp.async, also across two slabs (KS = 64)
+    "D126_two_slabs": (22, 160, -63, 62, 1, 2, 3.0, 10.0, 0.0, 1.0),
+    "D14_rho3": (30, 77, -7, 6, 2, 3, 3.0, 10.0, 0.02, 1.0),
 }
 
 
