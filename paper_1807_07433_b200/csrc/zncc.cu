@@ -144,7 +144,9 @@ struct ZnccGeom {
 __host__ __device__ inline ZnccGeom zncc_geom(int p, int D) {
   ZnccGeom g;
   const int NJ = ZX + 2 * p;
-  g.NRING = 2 * p + 2;                                   // image rows y-1 .. y+2p
+  // image rows y-1 .. y+2p being read, plus the one committed for the next row into
+  // the slot of y-2 (last read one iteration earlier): one barrier per row
+  g.NRING = 2 * p + 3;
   g.FC = ((ZTX + 2 * p + 3) / 4) * 4 + 4;
   g.gpad = (4 - (D & 3)) & 3;
   g.GC = ((ZTX + 2 * p + D - 1 + g.gpad + 3) / 4) * 4 + 8;
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
   // exact integer -> float for 0 <= v < 2^23 without the XU pipe
   auto u2f = [](uint32_t v) { return __uint_as_float(0x4B000000u | v) - 8388608.0f; };
   auto commit = [&](int t_img, int y_st) {
-    const int slot = t_img % (2 * P + 2);
+    const int slot = t_img % (2 * P + 3);
     if (t_img >= 0) {
 #pragma unroll
       for (int u = 0; u < NPI; u++) {
@@ -303,7 +305,7 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
     for (int qp = 0; qp < NQP; qp++) V2[j][qp] = make_float2(0.f, 0.f);
 
   auto accumulate_row = [&](int t, bool subtract) {
-    const int slot = t % (2 * P + 2);
+    const int slot = t % (2 * P + 3);
     float f[NF4 * 4], ge[NG4 * 4], go[NG4 * 4];
     const float4* fr = reinterpret_cast<const float4*>(Fs + slot * gm.FC + f_start);
     const float4* gr = reinterpret_cast<const float4*>(Gs + slot * gm.GROW + grun);
@@ -420,7 +422,8 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
         }
       }
     }
-    __syncthreads();   // ring slot of row y - 1 and St[(y + 1) & 1] are free
+    // the ring slot of row y - 2 and St[(y + 1) & 1] were last read in iteration
+    // y - 1, which every thread finished before the previous barrier
     if (more) commit(y + 1 + 2 * P, y + 1);
     __syncthreads();
   }
