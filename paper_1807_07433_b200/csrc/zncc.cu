@@ -129,7 +129,7 @@ cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* im
 constexpr int ZX = 4;     // columns per thread
 constexpr int ZR = 8;     // disparities per thread (4 packed pairs)
 constexpr int ZTX = 64;   // columns per CTA (16 column groups)
-constexpr int ZBY = 96;   // output rows per CTA
+constexpr int ZBY = 72;   // output rows per CTA (measured: 72 beats 48/60/80/90/96/144 at c5)
 
 // Shared-memory rows are stored "oriented": the G-side image row and G-side
 // statistics run so that, for a thread, the G entry of disparity q + 1 follows
