@@ -31,7 +31,7 @@ namespace rsr {
 // image, holds mask == 0 (warp-invalid, reading 7) or is constant
 // (exact integer test, reading 6).
 // ---------------------------------------------------------------------------
-constexpr int ST_TX = 64, ST_TY = 16;
+constexpr int ST_TX = 64, ST_TY = 32;   // 32 rows: 47 KB of shared memory at p = 3 (< 48 KB)
 
 template <int p>
 __global__ void __launch_bounds__(256) k_block_stats(int H, int W,
@@ -109,8 +109,17 @@ cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* im
   const size_t smem = sizeof(int) * (size_t)(2 * TR * TC + 3 * ST_TY * TC);
   dim3 grid((W + ST_TX - 1) / ST_TX, (H + ST_TY - 1) / ST_TY, B);
   switch (p) {
-#define RSR_BS(PP) \
-  case PP: k_block_stats<PP><<<grid, 256, smem, st>>>(H, W, img, mask, S, inv); break;
+#define RSR_BS(PP)                                                                              \
+  case PP: {                                                                                    \
+    if (smem > 48 * 1024) {                                                                     \
+      const cudaError_t e = cudaFuncSetAttribute(k_block_stats<PP>,                            \
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                                 (int)smem);                                    \
+      if (e != cudaSuccess) return e;                                                           \
+    }                                                                                           \
+    k_block_stats<PP><<<grid, 256, smem, st>>>(H, W, img, mask, S, inv);                        \
+    break;                                                                                      \
+  }
     RSR_BS(1) RSR_BS(2) RSR_BS(3) RSR_BS(4) RSR_BS(5) RSR_BS(6) RSR_BS(7)
 #undef RSR_BS
     default: return cudaErrorInvalidValue;

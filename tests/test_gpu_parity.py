@@ -233,6 +233,8 @@ EDGE_CASES = {
     # D % 4 == 2 rows staged by 8-byte cp.async, also across two slabs (KS = 64)
     "D126_two_slabs": (22, 160, -63, 62, 1, 2, 3.0, 10.0, 0.0, 1.0),
     "D14_rho3": (30, 77, -7, 6, 2, 3, 3.0, 10.0, 0.02, 1.0),
+    # largest NCC block (15x15): block statistics need > 48 KB of shared memory
+    "rho_block7": (44, 100, -4, 11, 7, 2, 2.0, 10.0, 0.0, 2.0),
 }
 
 
