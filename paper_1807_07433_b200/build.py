@@ -1,13 +1,18 @@
-"""Build librsr.so (all CUDA sources under csrc/) for sm_100a, in-tree."""
+"""Build librsr.so (all CUDA sources under csrc/) for sm_100a, in-tree.
+
+Each source compiles to its own object in parallel (the kernels of one file call
+no device code of another), then nvcc links the shared library."""
 import glob
 import os
 import subprocess
 import sys
+import tempfile
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "librsr.so")
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 
 def sources():
@@ -23,28 +28,46 @@ def up_to_date():
     return all(os.path.getmtime(d) <= t for d in deps)
 
 
+def _nvcc():
+    return os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _compile_link(out, defines=()):
+    """Objects in parallel, then one link; returns (ok, log)."""
+    with tempfile.TemporaryDirectory() as tmp:
+        def one(src):
+            obj = os.path.join(tmp, os.path.basename(src) + ".o")
+            cmd = [_nvcc()] + NVCC_FLAGS + ["-D" + d for d in defines] + ["-c", src, "-o", obj]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            return obj, r.returncode, " ".join(cmd) + "\n" + r.stdout + r.stderr
+        with ThreadPoolExecutor(max_workers=max(1, min(len(sources()), os.cpu_count() or 1))) as ex:
+            results = list(ex.map(one, sources()))
+        log = "".join(x[2] for x in results)
+        if any(x[1] != 0 for x in results):
+            return False, log
+        cmd = [_nvcc()] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", out] + [x[0] for x in results]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        return r.returncode == 0, log + " ".join(cmd) + "\n" + r.stdout + r.stderr
+
+
 def build(force=False, verbose=False, out=None, defines=()):
     """Compile every csrc/*.cu into one shared library (default: librsr.so)."""
     if out is not None:   # experiment build (tools/): always rebuilt
-        cmd = [os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")] + NVCC_FLAGS + \
-              ["-D" + d for d in defines] + ["-o", out] + sources()
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stderr)
+        ok, log = _compile_link(out, defines)
+        if not ok:
+            sys.stderr.write(log)
             raise RuntimeError("nvcc failed")
         return out
     if not force and up_to_date():
         return LIB
-    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc] + NVCC_FLAGS + ["-o", LIB] + sources()
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    ok, log = _compile_link(LIB)
     with open(os.path.join(HERE, "build_ptxas.log"), "w") as f:
-        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-    if r.returncode != 0:
-        sys.stderr.write(r.stderr)
+        f.write(log)
+    if not ok:
+        sys.stderr.write(log)
         raise RuntimeError("nvcc failed building librsr.so")
     if verbose:
-        print(r.stderr)
+        print(log)
     return LIB
 
 
