@@ -86,8 +86,9 @@ __global__ void __launch_bounds__(256) k_disparity(int H, int W, int d_lo, int D
   const bool vec4 = (D & 3) == 0;
   const int l = threadIdx.x % DG, g = threadIdx.x / DG, ng = blockDim.x / DG;
   const int Wr = (W + 4 * ng - 1) / (4 * ng) * (4 * ng);   // uniform trip count: every lane reaches the shuffles
-  // four pixels per group per iteration: eight 16-byte loads in flight per lane
-  constexpr int UP = 4;
+  // two pixels per group per iteration: four 16-byte loads in flight per lane
+  // (measured: 2 beats 1, 4 and 8 -- fewer registers, more resident CTAs)
+  constexpr int UP = 2;
   for (int u0 = g; u0 < Wr; u0 += UP * ng) {
     float bv[UP];
     int bk[UP];
