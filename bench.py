@@ -229,8 +229,9 @@ def main():
         fork = torch.cuda.Event(); fork.record(stream); side.wait_event(fork)
         with torch.cuda.stream(side):
             rsr.rsr_aggregate(pipe.vol_tar, pipe.warped, p.rho_agg, p.gamma_d, p.gamma_r, pipe.nan_tar,
-                              pipe.agg_tar)
-        rsr.rsr_aggregate(pipe.vol_ref, L, p.rho_agg, p.gamma_d, p.gamma_r, pipe.nan_ref, pipe.agg_ref)
+                              pipe.agg_tar, concurrency=2)
+        rsr.rsr_aggregate(pipe.vol_ref, L, p.rho_agg, p.gamma_d, p.gamma_r, pipe.nan_ref, pipe.agg_ref,
+                          concurrency=2)
         join = torch.cuda.Event(); join.record(side); stream.wait_event(join)
         if record:
             e = torch.cuda.Event(enable_timing=True); e.record(stream); ev["agg3"].append(e)

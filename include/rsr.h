@@ -125,11 +125,15 @@ int rsr_cost_volume(rsr_shape s, rsr_cost_params p, const uint8_t* ref,
 /*             slower).                                                       */
 /*   out     : float [B][H][W][D]; must not alias vol                         */
 /* Errors: RSR_E_ARG on NULL vol/guide/out, D < 1 or > 32767, rho < 0 or      */
-/* > 10, gamma_d <= 0 or NaN, gamma_r <= 0 or NaN.                            */
+/* > 10, gamma_d <= 0 or NaN, gamma_r <= 0 or NaN, concurrency < 0 or > 64.  */
 typedef struct {
   int32_t rho;      /* rho, aggregation half window (window = 2 rho + 1)      */
   float gamma_d;    /* spatial parameter of Eq. (9)                           */
   float gamma_r;    /* range parameter of Eq. (10), may be +inf               */
+  int32_t concurrency; /* scheduling hint: aggregations the caller keeps in    */
+                       /* flight together on other streams (0 or 1 = alone;   */
+                       /* the pipeline's two volumes = 2).  Chooses the grid, */
+                       /* never the result (bitwise independent of it).      */
 } rsr_agg_params;
 
 int rsr_aggregate(rsr_shape s, int32_t D, rsr_agg_params p, const float* vol,

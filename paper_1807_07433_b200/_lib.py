@@ -23,7 +23,8 @@ class RsrCostParams(ctypes.Structure):
 
 
 class RsrAggParams(ctypes.Structure):
-    _fields_ = [("rho", ctypes.c_int32), ("gamma_d", ctypes.c_float), ("gamma_r", ctypes.c_float)]
+    _fields_ = [("rho", ctypes.c_int32), ("gamma_d", ctypes.c_float), ("gamma_r", ctypes.c_float),
+                ("concurrency", ctypes.c_int32)]
 
 
 class RsrDispParams(ctypes.Structure):

@@ -605,7 +605,7 @@ static int sm_count() {
 }
 
 template <int RHO>
-static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, float gamma_r,
+static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, float gamma_r, int conc,
                                   const float* vol, const uint8_t* guide, const uint8_t* nan_map,
                                   float* out, cudaStream_t st) {
   const SlideGeom g1 = slide_geom(D, RHO);
@@ -619,14 +619,16 @@ static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, flo
   const bool small = g1.G <= (RHO <= 5 ? 4 : 2);
   const int minb = small ? 2 : 1;
   auto fits = [&](int R) { return minb == 1 || slide_geom(D, RHO, R).bytes <= 113 * 1024; };
-  // rows per CTA: minimise (waves of minb-CTAs-per-SM launches) x (rows + 2 rho warm-up)
+  // rows per CTA: minimise (waves of minb-CTAs-per-SM launches) x (rows + 2 rho warm-up),
+  // counting the CTAs of the conc aggregations the caller keeps in flight together
+  const long long inflight = conc > 1 ? conc : 1;
   int bestR = 0;
   double best = 1e300;
   for (int n = (H + SG_SEGMAX - 1) / SG_SEGMAX; n <= H; n++) {
     const int R = (H + n - 1) / n;
     if (R < 8 && n > 1) break;
     if (!fits(R)) continue;
-    const long long ctas = cols * ((H + R - 1) / R);
+    const long long ctas = cols * ((H + R - 1) / R) * inflight;
     const double cost = (double)((ctas + (long long)minb * nsm - 1) / ((long long)minb * nsm)) * (R + 2 * RHO);
     if (cost < best * 0.999) { best = cost; bestR = R; }
   }
@@ -657,11 +659,11 @@ static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, flo
 
 size_t aggregate_slide_smem(int D, int rho, int H) { (void)H; return slide_geom(D, rho).bytes; }
 
-cudaError_t launch_aggregate_slide(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r,
+cudaError_t launch_aggregate_slide(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r, int conc,
                                    const float* vol, const uint8_t* guide, const uint8_t* nan_map,
                                    float* out, cudaStream_t st) {
 #define RSR_S(R) \
-  case R: return slide_launch_t<R>(B, H, W, D, gamma_d, gamma_r, vol, guide, nan_map, out, st);
+  case R: return slide_launch_t<R>(B, H, W, D, gamma_d, gamma_r, conc, vol, guide, nan_map, out, st);
   switch (rho) {
     RSR_S(0) RSR_S(1) RSR_S(2) RSR_S(3) RSR_S(4) RSR_S(5) RSR_S(6) RSR_S(7)
     default:

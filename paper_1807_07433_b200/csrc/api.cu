@@ -85,11 +85,12 @@ int rsr_aggregate(rsr_shape s, int32_t D, rsr_agg_params p, const float* vol, co
   if (!shape_ok(s) || !vol || !guide || !out) return RSR_E_ARG;
   if (D < 1 || D > 32767 || p.rho < 0 || p.rho > 10) return RSR_E_ARG;
   if (!(p.gamma_d > 0.f) || std::isinf(p.gamma_d) || !(p.gamma_r > 0.f)) return RSR_E_ARG;
+  if (p.concurrency < 0 || p.concurrency > 64) return RSR_E_ARG;
   if (vol == out) return RSR_E_ARG;
   if ((s.height + 7) / 8 > 65535) return RSR_E_ARG;
   const long long nslab = (D + 63) / 64;
   if ((long long)s.batch * nslab > 65535) return RSR_E_ARG;
-  return launched(rsr::launch_aggregate(s.batch, s.height, s.width, D, p.rho, p.gamma_d, p.gamma_r,
+  return launched(rsr::launch_aggregate(s.batch, s.height, s.width, D, p.rho, p.gamma_d, p.gamma_r, p.concurrency,
                                         vol, guide, nan_map, out, as_stream(stream)));
 }
 

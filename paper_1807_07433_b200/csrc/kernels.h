@@ -27,13 +27,13 @@ cudaError_t launch_zncc(bool tar, int B, int H, int W, int rho_b, int d_lo, int 
 cudaError_t launch_nan_maps(int B, int H, int W, int d_lo, int D, const float* invL,
                             const float* invW, uint8_t* nan_ref, uint8_t* nan_tar, cudaStream_t st);
 
-cudaError_t launch_aggregate(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r,
+cudaError_t launch_aggregate(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r, int conc,
                              const float* vol, const uint8_t* guide, const uint8_t* nan_map,
                              float* out, cudaStream_t st);
 
 // sliding-window warp-specialised variant (rho <= 7); launch_aggregate dispatches to it
 cudaError_t launch_aggregate_slide(int B, int H, int W, int D, int rho, float gamma_d,
-                                   float gamma_r, const float* vol, const uint8_t* guide,
+                                   float gamma_r, int conc, const float* vol, const uint8_t* guide,
                                    const uint8_t* nan_map, float* out, cudaStream_t st);
 size_t aggregate_slide_smem(int D, int rho, int H);
 size_t aggregate_tiled_smem(int D, int rho);

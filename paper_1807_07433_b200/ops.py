@@ -89,8 +89,9 @@ def rsr_cost_volume(ref, warped, valid, rho_block, d_lo, d_hi, *, with_tar=True,
     return vol_ref, vol_tar, nan_ref, nan_tar
 
 
-def rsr_aggregate(vol, guide, rho, gamma_d, gamma_r, nan_map=None, out=None):
-    """Step 3 (Eqs. 8-10): aggregated volume float32 [B,H,W,D]."""
+def rsr_aggregate(vol, guide, rho, gamma_d, gamma_r, nan_map=None, out=None, concurrency=1):
+    """Step 3 (Eqs. 8-10): aggregated volume float32 [B,H,W,D].  concurrency: how many
+    aggregations the caller keeps in flight together (grid choice only)."""
     guide, s = _bhw(guide)
     B, H, W = guide.shape
     if vol.dim() == 3:
@@ -101,7 +102,7 @@ def rsr_aggregate(vol, guide, rho, gamma_d, gamma_r, nan_map=None, out=None):
     if nan_map is not None:
         nan_map, _ = _bhw(nan_map)
     check("rsr_aggregate", lib().rsr_aggregate(
-        s, D, RsrAggParams(rho, float(gamma_d), float(gamma_r)), _ptr(vol), _ptr(guide),
+        s, D, RsrAggParams(rho, float(gamma_d), float(gamma_r), int(concurrency)), _ptr(vol), _ptr(guide),
         _ptr(nan_map), _ptr(out), _stream()))
     return out
 

@@ -83,8 +83,9 @@ class StereoPipeline:
         self._side.wait_event(fork)
         with torch.cuda.stream(self._side):
             ops.rsr_aggregate(self.vol_tar, self.warped, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_tar,
-                              self.agg_tar)
-        ops.rsr_aggregate(self.vol_ref, left, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_ref, self.agg_ref)
+                              self.agg_tar, concurrency=2)
+        ops.rsr_aggregate(self.vol_ref, left, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_ref, self.agg_ref,
+                          concurrency=2)
         join = torch.cuda.Event()
         join.record(self._side)
         main.wait_event(join)

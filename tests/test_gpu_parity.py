@@ -315,3 +315,17 @@ def test_bad_arguments_return_codes(rsr):
     assert L.rsr_aggregate(RsrShape(1, 2, 2), 4, RsrAggParams(-1, 1.0, 1.0), p, p, None, p + 64, None) == 2
     assert L.rsr_aggregate(RsrShape(1, 2, 2), 4, RsrAggParams(1, 0.0, 1.0), p, p, None, p + 64, None) == 2
     assert L.rsr_aggregate(RsrShape(1, 2, 2), 4, RsrAggParams(1, 1.0, 1.0), p, p, None, p, None) == 2
+
+
+def test_aggregate_independent_of_concurrency_hint(rsr):
+    """The concurrency hint picks K3's row chunking only: bitwise equal results."""
+    cfg = synth.get_config("c2")
+    left, right, ab = synth.make_batch(cfg, [0, 1])
+    L = torch.from_numpy(left).cuda()
+    R = torch.from_numpy(right).cuda()
+    W_, M_, S_ = rsr.rsr_warp(R, torch.from_numpy(ab).cuda())
+    cl, cr, nl, nr = rsr.rsr_cost_volume(L, W_, M_, cfg.rho_block, cfg.d_lo, cfg.d_hi)
+    outs = [rsr.rsr_aggregate(cl, L, cfg.rho_agg, cfg.gamma_d, cfg.gamma_r, nl, concurrency=c) for c in (1, 2, 7)]
+    torch.cuda.synchronize()
+    for o in outs[1:]:
+        assert torch.equal(torch.nan_to_num(outs[0], nan=-7.0), torch.nan_to_num(o, nan=-7.0))
