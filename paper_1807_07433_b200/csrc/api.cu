@@ -68,12 +68,17 @@ int rsr_cost_volume(rsr_shape s, rsr_cost_params p, const uint8_t* ref, const ui
                                           SL, iL, st);
   if (e == cudaSuccess)
     e = rsr::launch_block_stats(s.batch, s.height, s.width, p.rho_block, warped, valid, SW, iW, st);
-  if (e == cudaSuccess)
-    e = rsr::launch_zncc(false, s.batch, s.height, s.width, p.rho_block, p.d_lo, (int)D, ref,
-                         warped, SL, iL, SW, iW, vol_ref, st);
-  if (e == cudaSuccess && vol_tar)
-    e = rsr::launch_zncc(true, s.batch, s.height, s.width, p.rho_block, p.d_lo, (int)D, ref,
-                         warped, SL, iL, SW, iW, vol_tar, st);
+  if (e == cudaSuccess && vol_tar && 2LL * s.batch <= 65535)   // both volumes, one grid
+    e = rsr::launch_zncc_pair(s.batch, s.height, s.width, p.rho_block, p.d_lo, (int)D, ref, warped, SL, iL,
+                              SW, iW, vol_ref, vol_tar, st);
+  else {
+    if (e == cudaSuccess)
+      e = rsr::launch_zncc(false, s.batch, s.height, s.width, p.rho_block, p.d_lo, (int)D, ref,
+                           warped, SL, iL, SW, iW, vol_ref, st);
+    if (e == cudaSuccess && vol_tar)
+      e = rsr::launch_zncc(true, s.batch, s.height, s.width, p.rho_block, p.d_lo, (int)D, ref,
+                           warped, SL, iL, SW, iW, vol_tar, st);
+  }
   if (e == cudaSuccess)
     e = rsr::launch_nan_maps(s.batch, s.height, s.width, p.d_lo, (int)D, iL, iW, nan_ref,
                              vol_tar ? nan_tar : nullptr, st);

@@ -18,6 +18,10 @@ cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* im
 
 // NCC volume in [B][H][W][D] layout. tar=false: vol[v][u][k] = c(u, v, r);
 // tar=true: vol[v][u'][k] = c(u'+r, v, r).
+// both volumes in one launch (grid of 2B frames)
+cudaError_t launch_zncc_pair(int B, int H, int W, int rho_b, int d_lo, int D, const uint8_t* ref,
+                             const uint8_t* warped, const int32_t* SL, const float* invL, const int32_t* SW,
+                             const float* invW, float* vol_ref, float* vol_tar, cudaStream_t st);
 cudaError_t launch_zncc(bool tar, int B, int H, int W, int rho_b, int d_lo, int D,
                         const uint8_t* ref, const uint8_t* warped, const int32_t* SL,
                         const float* invL, const int32_t* SW, const float* invW, float* vol,

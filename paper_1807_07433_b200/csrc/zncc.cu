@@ -174,8 +174,9 @@ __host__ __device__ inline size_t zncc_smem(int p, int D) {
   return sizeof(float) * ((size_t)g.NRING * (g.FC + 2 * g.GROW) + 2 * (2 * ZTX + 4 * (size_t)g.SROW2));
 }
 
+// One CTA of the volume kernel for frame b (the kernels below pick b and TAR).
 template <int P, bool TAR>
-__global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(int H, int W, int d_lo, int D, int Dst, int koff,
+__device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, int Dst, int koff,
                                               const uint8_t* __restrict__ ref,
                                               const uint8_t* __restrict__ warped,
                                               const int32_t* __restrict__ SLg,
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
   float* St = Gs1 + gm.NRING * gm.GROW;              // [2][sF ZTX | iF ZTX | sG | sG1 | iG | iG1]
   const int SROW = 2 * ZTX + 4 * gm.SROW2;
 
-  const int b = blockIdx.z, x0 = blockIdx.x * ZTX, y0 = blockIdx.y * ZBY;
+  const int x0 = blockIdx.x * ZTX, y0 = blockIdx.y * ZBY;
   const int d_hi = d_lo + D - 1;
   const size_t ibase = (size_t)b * H * W;
   // F = image at the fixed column; G = image at the shifted column x -/+ r.
@@ -438,6 +439,42 @@ __global__ void __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1))) k_zncc(i
   }
 }
 
+#define RSR_ZNCC_BOUNDS __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1)))
+
+template <int P, bool TAR>
+__global__ void RSR_ZNCC_BOUNDS k_zncc(int H, int W, int d_lo, int D, int Dst, int koff, const uint8_t* ref,
+                                       const uint8_t* warped, const int32_t* SLg, const float* invLg,
+                                       const int32_t* SWg, const float* invWg, float* vol) {
+  zncc_cta<P, TAR>(blockIdx.z, H, W, d_lo, D, Dst, koff, ref, warped, SLg, invLg, SWg, invWg, vol);
+}
+
+// Both volumes in one launch (frames [0, B) -> reference, [B, 2B) -> target): one
+// grid twice as long, so the two halves fill each other's last wave.
+template <int P>
+__global__ void RSR_ZNCC_BOUNDS k_zncc_pair(int B, int H, int W, int d_lo, int D, int Dst, int koff,
+                                            const uint8_t* ref, const uint8_t* warped, const int32_t* SLg,
+                                            const float* invLg, const int32_t* SWg, const float* invWg,
+                                            float* vol_ref, float* vol_tar) {
+  if ((int)blockIdx.z < B)
+    zncc_cta<P, false>(blockIdx.z, H, W, d_lo, D, Dst, koff, ref, warped, SLg, invLg, SWg, invWg, vol_ref);
+  else
+    zncc_cta<P, true>(blockIdx.z - B, H, W, d_lo, D, Dst, koff, ref, warped, SLg, invLg, SWg, invWg, vol_tar);
+}
+
+template <int P>
+static cudaError_t zncc_pair_launch_t(int B, int H, int W, int d_lo, int D, int Dst, int koff, const uint8_t* ref,
+                                      const uint8_t* warped, const int32_t* SL, const float* invL,
+                                      const int32_t* SW, const float* invW, float* vol_ref, float* vol_tar,
+                                      cudaStream_t st) {
+  const size_t smem = zncc_smem(P, D);
+  auto kern = k_zncc_pair<P>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) { cudaGetLastError(); return e; }
+  dim3 grid((W + ZTX - 1) / ZTX, (H + ZBY - 1) / ZBY, 2 * B);
+  kern<<<grid, 128, smem, st>>>(B, H, W, d_lo, D, Dst, koff, ref, warped, SL, invL, SW, invW, vol_ref, vol_tar);
+  return cudaGetLastError();
+}
+
 template <int P, bool TAR>
 static cudaError_t zncc_launch_t(int B, int H, int W, int d_lo, int D, int Dst, int koff,
                                  const uint8_t* ref,
@@ -543,6 +580,31 @@ cudaError_t launch_nan_maps(int B, int H, int W, int d_lo, int D, const float* i
   }
   k_nan_maps<<<dim3(H, B), 256, smem, st>>>(H, W, d_lo, D, invL, invW, nan_ref, nan_tar);
   return cudaGetLastError();
+}
+
+cudaError_t launch_zncc_pair(int B, int H, int W, int rho_b, int d_lo, int D, const uint8_t* ref,
+                             const uint8_t* warped, const int32_t* SL, const float* invL, const int32_t* SW,
+                             const float* invW, float* vol_ref, float* vol_tar, cudaStream_t st) {
+  constexpr int SLAB = 64;
+  if (2LL * B > 65535) return cudaErrorInvalidValue;
+  for (int k0 = 0; k0 < D; k0 += SLAB) {
+    const int Ds = D - k0 < SLAB ? D - k0 : SLAB;
+    const int dl = d_lo + k0;
+    cudaError_t e;
+#define RSR_Z(PP)                                                                                  \
+  case PP:                                                                                         \
+    e = zncc_pair_launch_t<PP>(B, H, W, dl, Ds, D, k0, ref, warped, SL, invL, SW, invW, vol_ref,   \
+                               vol_tar, st);                                                       \
+    break;
+    switch (rho_b) {
+      RSR_Z(1) RSR_Z(2) RSR_Z(3) RSR_Z(4) RSR_Z(5) RSR_Z(6) RSR_Z(7)
+      default:
+        return cudaErrorInvalidValue;
+    }
+#undef RSR_Z
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_zncc(bool tar, int B, int H, int W, int rho_b, int d_lo, int D,
