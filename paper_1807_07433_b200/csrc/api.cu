@@ -64,10 +64,18 @@ int rsr_cost_volume(rsr_shape s, rsr_cost_params p, const uint8_t* ref, const ui
   int32_t* SW = reinterpret_cast<int32_t*>(ws + 2 * chunk);
   float* iW = reinterpret_cast<float*>(ws + 3 * chunk);
   cudaStream_t st = as_stream(stream);
-  cudaError_t e = rsr::launch_block_stats(s.batch, s.height, s.width, p.rho_block, ref, nullptr,
-                                          SL, iL, st);
-  if (e == cudaSuccess)
-    e = rsr::launch_block_stats(s.batch, s.height, s.width, p.rho_block, warped, valid, SW, iW, st);
+  // both images' block statistics in one grid (two grids past 65535 / 2 frames)
+  cudaError_t e;
+  if (2LL * s.batch <= 65535) {
+    e = rsr::launch_block_stats(s.batch, s.height, s.width, p.rho_block, ref, nullptr, SL, iL, warped, valid,
+                                SW, iW, st);
+  } else {
+    e = rsr::launch_block_stats(s.batch, s.height, s.width, p.rho_block, ref, nullptr, SL, iL, nullptr,
+                                nullptr, nullptr, nullptr, st);
+    if (e == cudaSuccess)
+      e = rsr::launch_block_stats(s.batch, s.height, s.width, p.rho_block, warped, valid, SW, iW, nullptr,
+                                  nullptr, nullptr, nullptr, st);
+  }
   if (e == cudaSuccess && vol_tar && 2LL * s.batch <= 65535)   // both volumes, one grid
     e = rsr::launch_zncc_pair(s.batch, s.height, s.width, p.rho_block, p.d_lo, (int)D, ref, warped, SL, iL,
                               SW, iW, vol_ref, vol_tar, st);

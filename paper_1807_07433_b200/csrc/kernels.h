@@ -13,8 +13,9 @@ cudaError_t launch_warp(int B, int H, int W, const double* ab, const uint8_t* ta
 // Per-pixel block statistics for the NCC normalisation: S = sum i (int32),
 // inv = 1/sqrt(n*sum i^2 - S^2) (fp32, NaN if the block leaves the image, touches
 // mask==0 or is constant).  mask may be null.
-cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* img,
-                               const uint8_t* mask, int32_t* S, float* inv, cudaStream_t st);
+cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* img0, const uint8_t* mask0,
+                               int32_t* S0, float* inv0, const uint8_t* img1, const uint8_t* mask1, int32_t* S1,
+                               float* inv1, cudaStream_t st);
 
 // NCC volume in [B][H][W][D] layout. tar=false: vol[v][u][k] = c(u, v, r);
 // tar=true: vol[v][u'][k] = c(u'+r, v, r).

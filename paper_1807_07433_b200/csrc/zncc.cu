@@ -33,12 +33,20 @@ namespace rsr {
 // ---------------------------------------------------------------------------
 constexpr int ST_TX = 64, ST_TY = 32;   // 32 rows: 47 KB of shared memory at p = 3 (< 48 KB)
 
+// Both images in one grid: frames [0, B) are img0 (mask0, S0, inv0), [B, 2B) img1.
 template <int p>
-__global__ void __launch_bounds__(256) k_block_stats(int H, int W,
-                                                     const uint8_t* __restrict__ img,
-                                                     const uint8_t* __restrict__ mask,
-                                                     int32_t* __restrict__ Sout,
-                                                     float* __restrict__ inv) {
+__global__ void __launch_bounds__(256) k_block_stats(int B, int H, int W,
+                                                     const uint8_t* __restrict__ img0,
+                                                     const uint8_t* __restrict__ mask0,
+                                                     int32_t* __restrict__ S0, float* __restrict__ inv0,
+                                                     const uint8_t* __restrict__ img1,
+                                                     const uint8_t* __restrict__ mask1,
+                                                     int32_t* __restrict__ S1, float* __restrict__ inv1) {
+  const bool second = (int)blockIdx.z >= B;
+  const uint8_t* __restrict__ img = second ? img1 : img0;
+  const uint8_t* __restrict__ mask = second ? mask1 : mask0;
+  int32_t* __restrict__ Sout = second ? S1 : S0;
+  float* __restrict__ inv = second ? inv1 : inv0;
   extern __shared__ int st_smem[];
   const int TC = ST_TX + 2 * p, TR = ST_TY + 2 * p;
   int* pix = st_smem;                // [TR][TC] value
@@ -46,7 +54,7 @@ __global__ void __launch_bounds__(256) k_block_stats(int H, int W,
   int* cS = msk + TR * TC;           // [ST_TY][TC] vertical sums
   int* cSS = cS + ST_TY * TC;
   int* cM = cSS + ST_TY * TC;
-  const int b = blockIdx.z, x0 = blockIdx.x * ST_TX, y0 = blockIdx.y * ST_TY;
+  const int b = second ? (int)blockIdx.z - B : (int)blockIdx.z, x0 = blockIdx.x * ST_TX, y0 = blockIdx.y * ST_TY;
   const size_t base = (size_t)b * H * W;
   constexpr int UNR = 8;   // independent loads in flight per thread
   for (int i0 = threadIdx.x; i0 < TR * TC; i0 += UNR * blockDim.x) {
@@ -102,12 +110,15 @@ __global__ void __launch_bounds__(256) k_block_stats(int H, int W,
   }
 }
 
-cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* img,
-                               const uint8_t* mask, int32_t* S, float* inv, cudaStream_t st) {
+cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* img0, const uint8_t* mask0,
+                               int32_t* S0, float* inv0, const uint8_t* img1, const uint8_t* mask1, int32_t* S1,
+                               float* inv1, cudaStream_t st) {
   const int p = rho_b;
   const int TC = ST_TX + 2 * p, TR = ST_TY + 2 * p;
   const size_t smem = sizeof(int) * (size_t)(2 * TR * TC + 3 * ST_TY * TC);
-  dim3 grid((W + ST_TX - 1) / ST_TX, (H + ST_TY - 1) / ST_TY, B);
+  const int nimg = img1 ? 2 : 1;
+  if ((long long)nimg * B > 65535) return cudaErrorInvalidValue;
+  dim3 grid((W + ST_TX - 1) / ST_TX, (H + ST_TY - 1) / ST_TY, nimg * B);
   switch (p) {
 #define RSR_BS(PP)                                                                              \
   case PP: {                                                                                    \
@@ -117,7 +128,7 @@ cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* im
                                                  (int)smem);                                    \
       if (e != cudaSuccess) return e;                                                           \
     }                                                                                           \
-    k_block_stats<PP><<<grid, 256, smem, st>>>(H, W, img, mask, S, inv);                        \
+    k_block_stats<PP><<<grid, 256, smem, st>>>(B, H, W, img0, mask0, S0, inv0, img1, mask1, S1, inv1); \
     break;                                                                                      \
   }
     RSR_BS(1) RSR_BS(2) RSR_BS(3) RSR_BS(4) RSR_BS(5) RSR_BS(6) RSR_BS(7)

@@ -37,14 +37,14 @@ class StereoParams:
 class StereoPipeline:
     """Pre-allocated buffers for a [B,H,W] batch; run() enqueues the whole path.
 
-    Kernel launches per run(): warp 1; cost volume 2 block-stats + ceil(D/64)
+    Kernel launches per run(): warp 1; cost volume 1 block-stats (both images) + ceil(D/64)
     NCC slabs (both volumes per grid) + 1 NaN-summary; aggregation 2 (rho <= 7); disparity 1;
     reconstruction 1 (see launches()).
     """
 
     @staticmethod
     def launches(D: int) -> int:
-        return 1 + (2 + (D + 63) // 64 + 1) + 2 + 1 + 1   # both NCC volumes in one grid per slab
+        return 1 + (1 + (D + 63) // 64 + 1) + 2 + 1 + 1   # both images / volumes in one grid each
 
     def __init__(self, B, H, W, params: StereoParams, device="cuda"):
         self.B, self.H, self.W, self.p = B, H, W, params
