@@ -140,6 +140,12 @@ int rsr_aggregate(rsr_shape s, int32_t D, rsr_agg_params p, const float* vol,
                   const uint8_t* guide, const uint8_t* nan_map, float* out,
                   void* stream);
 
+/* Introspection (tests, tools): the number of output rows R per CTA that       */
+/* rsr_aggregate uses for these arguments (row chunks [0,R), [R,2R), ...; the    */
+/* result never depends on R), 0 for the rho > 7 tiled kernel, -1 on invalid    */
+/* arguments.  Host-only; enqueues nothing.                                      */
+int32_t rsr_aggregate_rows(rsr_shape s, int32_t D, rsr_agg_params p);
+
 /* ------------------------------------------------------------------------ */
 /* Steps 4-5 — WTA, left-right consistency, parabola subpixel and            */
 /* post-processing.                                              */

@@ -64,6 +64,8 @@ def lib() -> ctypes.CDLL:
         L.rsr_cost_workspace_size.restype = ctypes.c_size_t
         L.rsr_cost_volume.argtypes = [RsrShape, RsrCostParams, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]
         L.rsr_aggregate.argtypes = [RsrShape, ctypes.c_int32, RsrAggParams, P, P, P, P, P]
+        L.rsr_aggregate_rows.argtypes = [RsrShape, ctypes.c_int32, RsrAggParams]
+        L.rsr_aggregate_rows.restype = ctypes.c_int32
         L.rsr_disparity.argtypes = [RsrShape, RsrDispParams, P, P, P, P, P, P, P]
         L.rsr_reconstruct.argtypes = [RsrShape, RsrRig, P, P, P]
         L.rsr_road_workspace_size.argtypes = [RsrShape, RsrRoadParams]

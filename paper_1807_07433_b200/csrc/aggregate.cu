@@ -43,13 +43,11 @@ struct AggGeom {
   size_t off_cost, off_w, off_guide, off_dpart, off_bar, bytes;
 };
 
-__host__ __device__ inline AggGeom agg_geom(int D, int rho) {
+__host__ __device__ inline AggGeom agg_geom_cw(int D, int rho, int n_cw) {
   AggGeom g;
   const int ks = D < 128 ? D : 128;
   g.n_kg = (ks + AG_KT - 1) / AG_KT;
-  g.n_cw = 8 / g.n_kg;
-  if (g.n_cw > 4) g.n_cw = 4;
-  if (g.n_cw < 1) g.n_cw = 1;
+  g.n_cw = n_cw;
   g.TX = 32 * g.n_cw;
   g.KS = g.n_kg * AG_KT;
   g.DPAD = g.KS + 4;
@@ -66,6 +64,19 @@ __host__ __device__ inline AggGeom agg_geom(int D, int rho) {
   o = (o + 15) & ~size_t(15);
   g.off_bar = o;  o += 8 * AG_NST + 16;
   g.bytes = o;
+  return g;
+}
+
+// Column warps per CTA: up to 4 (8 warps with the disparity groups), fewer where the
+// weight stage of a wide window would not fit the 227 KB of shared memory (rho 9-10).
+__host__ __device__ inline AggGeom agg_geom(int D, int rho) {
+  const int ks = D < 128 ? D : 128;
+  const int n_kg = (ks + AG_KT - 1) / AG_KT;
+  int n_cw = 8 / n_kg;
+  if (n_cw > 4) n_cw = 4;
+  if (n_cw < 1) n_cw = 1;
+  AggGeom g = agg_geom_cw(D, rho, n_cw);
+  while (g.bytes > 227 * 1024 && n_cw > 1) g = agg_geom_cw(D, rho, --n_cw);
   return g;
 }
 
@@ -285,9 +296,8 @@ static cudaError_t aggregate_launch_t(int B, int H, int W, int D, float gamma_d,
                                       const uint8_t* nan_map, float* out, cudaStream_t st) {
   const AggGeom g = agg_geom(D, RHO);
   auto kern = k_aggregate<RHO>;
-  cudaError_t e =
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.bytes);
-  if (e != cudaSuccess) { cudaGetLastError(); return e; }
+  cudaError_t e = smem_optin((const void*)kern, g.bytes);
+  if (e != cudaSuccess) return e;
   const float log2e = 1.4426950408889634f;
   const float kd = -log2e / (gamma_d * gamma_d);
   const float kr = std::isinf(gamma_r) ? 0.f : -log2e / (gamma_r * gamma_r);

@@ -604,23 +604,23 @@ static int sm_count() {
   return n;
 }
 
-template <int RHO>
-static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, float gamma_r, int conc,
-                                  const float* vol, const uint8_t* guide, const uint8_t* nan_map,
-                                  float* out, cudaStream_t st) {
-  const SlideGeom g1 = slide_geom(D, RHO);
-  SlideArgs A;
-  A.B = B; A.H = H; A.W = W; A.D = D;
+// Row chunk R of one launch: minimise (waves of minb-CTAs-per-SM launches) x (R + 2 rho
+// warm-up rows), counting the CTAs of the conc aggregations the caller keeps in flight
+// together.  minb = 2 (two CTAs per SM) for small slabs whose guide tile of R rows leaves
+// room for two (at most 113 KB each).
+struct SlidePlan {
+  int R, minb;
+  bool compact;
+  size_t bytes;
+};
+
+static SlidePlan slide_plan(int B, int H, int W, int D, int rho, int conc, int nsm) {
+  const SlideGeom g1 = slide_geom(D, rho);
   const int nstrips = (W + 31) / 32;
   const long long cols = (long long)nstrips * B * g1.nslab;
-  const int nsm = sm_count();
-  // two CTAs per SM for small slabs (few consumer warps), if the guide tile of R rows
-  // leaves room for two: at most 113 KB each
-  const bool small = g1.G <= (RHO <= 5 ? 4 : 2);
+  const bool small = g1.G <= (rho <= 5 ? 4 : 2);
   const int minb = small ? 2 : 1;
-  auto fits = [&](int R) { return minb == 1 || slide_geom(D, RHO, R).bytes <= 113 * 1024; };
-  // rows per CTA: minimise (waves of minb-CTAs-per-SM launches) x (rows + 2 rho warm-up),
-  // counting the CTAs of the conc aggregations the caller keeps in flight together
+  auto fits = [&](int R) { return minb == 1 || slide_geom(D, rho, R).bytes <= 113 * 1024; };
   const long long inflight = conc > 1 ? conc : 1;
   int bestR = 0;
   double best = 1e300;
@@ -629,7 +629,7 @@ static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, flo
     if (R < 8 && n > 1) break;
     if (!fits(R)) continue;
     const long long ctas = cols * ((H + R - 1) / R) * inflight;
-    const double cost = (double)((ctas + (long long)minb * nsm - 1) / ((long long)minb * nsm)) * (R + 2 * RHO);
+    const double cost = (double)((ctas + (long long)minb * nsm - 1) / ((long long)minb * nsm)) * (R + 2 * rho);
     if (cost < best * 0.999) { best = cost; bestR = R; }
   }
   if (const char* e = getenv("RSR_K3_ROWS")) {   // experiment hook (tools/): force R
@@ -637,23 +637,44 @@ static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, flo
     if (r >= 8 && r <= SG_SEGMAX && fits(r)) bestR = r;
   }
   if (bestR == 0) bestR = 8;
-  A.R = bestR;
+  SlidePlan p;
+  p.R = bestR;
+  p.minb = minb;
+  // compact cost rows (one bulk copy per row) where D < KS and rows stay aligned; the
+  // compact kernels spill a little more, so D == KS keeps the padded layout
+  p.compact = small && g1.nslab == 1 && (D & 3) == 0 && D < g1.KS;
+  p.bytes = minb == 1 ? g1.bytes : slide_geom(D, rho, bestR).bytes;
+  return p;
+}
+
+int aggregate_plan_rows(int B, int H, int W, int D, int rho, int conc) {
+  if (rho > 7) return 0;   // tiled kernel (aggregate.cu): no row chunks
+  return slide_plan(B, H, W, D, rho, conc, sm_count()).R;
+}
+
+template <int RHO>
+static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, float gamma_r, int conc,
+                                  const float* vol, const uint8_t* guide, const uint8_t* nan_map,
+                                  float* out, cudaStream_t st) {
+  const SlideGeom g1 = slide_geom(D, RHO);
+  const SlidePlan plan = slide_plan(B, H, W, D, RHO, conc, sm_count());
+  SlideArgs A;
+  A.B = B; A.H = H; A.W = W; A.D = D;
+  const int nstrips = (W + 31) / 32;
+  const long long cols = (long long)nstrips * B * g1.nslab;
+  A.R = plan.R;
   A.nstrips = nstrips;
   const float log2e = 1.4426950408889634f;
   A.kd = -log2e / (gamma_d * gamma_d);
   A.kr = std::isinf(gamma_r) ? -1e-30f : -log2e / (gamma_r * gamma_r);
   A.vol = vol; A.guide = guide; A.nan_map = nan_map; A.out = out;
-  const long long nblk = cols * ((H + bestR - 1) / bestR);
+  const long long nblk = cols * ((H + plan.R - 1) / plan.R);
   if (nblk > 0x7fffffffLL) return cudaErrorInvalidValue;
-  const size_t bytes = minb == 1 ? g1.bytes : slide_geom(D, RHO, bestR).bytes;
-  // compact cost rows (one bulk copy per row) where D < KS and rows stay aligned; the
-  // compact kernels spill a little more, so D == KS keeps the padded layout
-  const bool compact = small && g1.nslab == 1 && (D & 3) == 0 && D < g1.KS;
-  auto kern = minb == 1 ? k_aggregate_slide<RHO, 1, false>
-                        : (compact ? k_aggregate_slide<RHO, 2, true> : k_aggregate_slide<RHO, 2, false>);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e != cudaSuccess) { cudaGetLastError(); return e; }
-  kern<<<(unsigned)nblk, 32 * (g1.G + SG_NPROD), bytes, st>>>(A);
+  auto kern = plan.minb == 1 ? k_aggregate_slide<RHO, 1, false>
+                             : (plan.compact ? k_aggregate_slide<RHO, 2, true> : k_aggregate_slide<RHO, 2, false>);
+  cudaError_t e = smem_optin((const void*)kern, plan.bytes);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)nblk, 32 * (g1.G + SG_NPROD), plan.bytes, st>>>(A);
   return cudaGetLastError();
 }
 

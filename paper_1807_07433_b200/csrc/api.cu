@@ -107,6 +107,11 @@ int rsr_aggregate(rsr_shape s, int32_t D, rsr_agg_params p, const float* vol, co
                                         vol, guide, nan_map, out, as_stream(stream)));
 }
 
+int32_t rsr_aggregate_rows(rsr_shape s, int32_t D, rsr_agg_params p) {
+  if (!shape_ok(s) || D < 1 || D > 32767 || p.rho < 0 || p.rho > 10) return -1;
+  return rsr::aggregate_plan_rows(s.batch, s.height, s.width, D, p.rho, p.concurrency);
+}
+
 int rsr_disparity(rsr_shape s, rsr_disp_params p, const float* agg_ref, const float* agg_tar,
                   const int32_t* shift, float* disparity, int16_t* wta_ref, int16_t* wta_tar,
                   void* stream) {

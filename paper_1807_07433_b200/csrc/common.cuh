@@ -1,6 +1,9 @@
 // Shared device helpers for the rsr kernels (sm_100a).
 #pragma once
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <cuda_runtime.h>
 
 #define RSR_DEVINL __device__ __forceinline__
@@ -131,6 +134,30 @@ RSR_DEVINL void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, u
           smem_u32(dst_smem)),
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` (host).  The
+// limit is a property of the kernel, not of one launch, so it only ever grows
+// (monotonic maximum per kernel and device, under a mutex): a concurrent call
+// that needs less can never have its limit lowered under it (include/rsr.h:
+// calls on different streams and host threads are safe).
+inline cudaError_t smem_optin(const void* kern, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> granted;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& g = granted[{kern, dev}];
+  if (g >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return e;
+  }
+  g = bytes;
+  return cudaSuccess;
 }
 
 }  // namespace rsr

@@ -149,11 +149,8 @@ cudaError_t launch_disparity(int B, int H, int W, int d_lo, int D, int tol, int 
                              const float* agg_ref, const float* agg_tar, const int32_t* shift,
                              float* disp, int16_t* wta_ref, int16_t* wta_tar, cudaStream_t st) {
   const size_t smem = sizeof(int16_t) * (size_t)W;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_disparity, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-  }
+  const cudaError_t e = smem_optin((const void*)k_disparity, smem);
+  if (e != cudaSuccess) return e;
   dim3 grid(H, B);
   k_disparity<<<grid, 256, smem, st>>>(H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, shift, disp,
                                        wta_ref, wta_tar);

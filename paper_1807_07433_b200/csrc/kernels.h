@@ -41,6 +41,8 @@ cudaError_t launch_aggregate_slide(int B, int H, int W, int D, int rho, float ga
                                    float gamma_r, int conc, const float* vol, const uint8_t* guide,
                                    const uint8_t* nan_map, float* out, cudaStream_t st);
 size_t aggregate_slide_smem(int D, int rho, int H);
+// output rows per CTA the sliding kernel uses for this call (0: tiled kernel, rho > 7)
+int aggregate_plan_rows(int B, int H, int W, int D, int rho, int conc);
 size_t aggregate_tiled_smem(int D, int rho);
 
 cudaError_t launch_disparity(int B, int H, int W, int d_lo, int D, int tol, int subpix,

@@ -122,12 +122,8 @@ cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* im
   switch (p) {
 #define RSR_BS(PP)                                                                              \
   case PP: {                                                                                    \
-    if (smem > 48 * 1024) {                                                                     \
-      const cudaError_t e = cudaFuncSetAttribute(k_block_stats<PP>,                            \
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                                                 (int)smem);                                    \
-      if (e != cudaSuccess) return e;                                                           \
-    }                                                                                           \
+    const cudaError_t e = smem_optin((const void*)k_block_stats<PP>, smem);                    \
+    if (e != cudaSuccess) return e;                                                             \
     k_block_stats<PP><<<grid, 256, smem, st>>>(B, H, W, img0, mask0, S0, inv0, img1, mask1, S1, inv1); \
     break;                                                                                      \
   }
@@ -479,8 +475,8 @@ static cudaError_t zncc_pair_launch_t(int B, int H, int W, int d_lo, int D, int 
                                       cudaStream_t st) {
   const size_t smem = zncc_smem(P, D);
   auto kern = k_zncc_pair<P>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) { cudaGetLastError(); return e; }
+  cudaError_t e = smem_optin((const void*)kern, smem);
+  if (e != cudaSuccess) return e;
   dim3 grid((W + ZTX - 1) / ZTX, (H + ZBY - 1) / ZBY, 2 * B);
   kern<<<grid, 128, smem, st>>>(B, H, W, d_lo, D, Dst, koff, ref, warped, SL, invL, SW, invW, vol_ref, vol_tar);
   return cudaGetLastError();
@@ -494,8 +490,8 @@ static cudaError_t zncc_launch_t(int B, int H, int W, int d_lo, int D, int Dst, 
                                  cudaStream_t st) {
   const size_t smem = zncc_smem(P, D);
   auto kern = k_zncc<P, TAR>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) { cudaGetLastError(); return e; }
+  cudaError_t e = smem_optin((const void*)kern, smem);
+  if (e != cudaSuccess) return e;
   // always 128 threads: (D <= 64) / 8 disparity groups x 16 column groups compute,
   // and all of them stream the rows (ZPF x 128 >= the longest row load list)
   const int threads = 128;
@@ -585,10 +581,8 @@ cudaError_t launch_nan_maps(int B, int H, int W, int d_lo, int D, const float* i
                             const float* invW, uint8_t* nan_ref, uint8_t* nan_tar, cudaStream_t st) {
   if (!nan_ref && !nan_tar) return cudaSuccess;
   const size_t smem = sizeof(int) * 2 * ((size_t)W + 1);
-  if (smem > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(k_nan_maps, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
+  const cudaError_t e = smem_optin((const void*)k_nan_maps, smem);
+  if (e != cudaSuccess) return e;
   k_nan_maps<<<dim3(H, B), 256, smem, st>>>(H, W, d_lo, D, invL, invW, nan_ref, nan_tar);
   return cudaGetLastError();
 }

@@ -1,10 +1,11 @@
-"""Python-level names of the five C-ABI calls (include/rsr.h), over torch CUDA
-tensors.  Each function checks dtype / device / shape / contiguity, allocates
-missing outputs with torch (device memory plumbing) and calls the library on
-the current torch CUDA stream.  No arithmetic of the method happens here."""
+"""Python-level names of the C-ABI calls (include/rsr.h), over torch CUDA
+tensors.  Each function checks the dtype, shape, device and contiguity of EVERY
+tensor argument, caller-supplied outputs and workspace included (the C ABI sees
+only pointers, so an undersized buffer would become an out-of-bounds device
+access), allocates missing outputs with torch (device memory plumbing) and
+calls the library on the current torch CUDA stream.  No arithmetic of the
+method happens here."""
 from __future__ import annotations
-
-import math
 
 import torch
 
@@ -29,6 +30,11 @@ def _stream():
 
 
 def _expect(t, dtype, shape, name):
+    """Check dtype and exact shape of a tensor argument (None passes: optional)."""
+    if t is None:
+        return
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"rsr: {name} must be a torch.Tensor")
     if t.dtype != dtype:
         raise TypeError(f"rsr: {name} must be {dtype}, got {t.dtype}")
     if tuple(t.shape) != tuple(shape):
@@ -53,6 +59,9 @@ def rsr_warp(target, alpha_beta, warped=None, valid=None, shift=None):
     warped = torch.empty_like(target) if warped is None else warped
     valid = torch.empty_like(target) if valid is None else valid
     shift = torch.empty((B, H), dtype=torch.int32, device=target.device) if shift is None else shift
+    _expect(warped, torch.uint8, (B, H, W), "warped")
+    _expect(valid, torch.uint8, (B, H, W), "valid")
+    _expect(shift, torch.int32, (B, H), "shift")
     check("rsr_warp", lib().rsr_warp(s, _ptr(alpha_beta), _ptr(target), _ptr(warped), _ptr(valid),
                                      _ptr(shift), _stream()))
     return warped, valid, shift
@@ -71,6 +80,10 @@ def rsr_cost_volume(ref, warped, valid, rho_block, d_lo, d_hi, *, with_tar=True,
     warped, _ = _bhw(warped)
     valid, _ = _bhw(valid)
     D = d_hi - d_lo + 1
+    if D < 1:
+        raise ValueError(f"rsr: empty search range [{d_lo}, {d_hi}]")
+    for t, name in ((ref, "ref"), (warped, "warped"), (valid, "valid")):
+        _expect(t, torch.uint8, (B, H, W), name)
     dev = ref.device
     if vol_ref is None:
         vol_ref = torch.empty((B, H, W, D), dtype=torch.float32, device=dev)
@@ -83,6 +96,12 @@ def rsr_cost_volume(ref, warped, valid, rho_block, d_lo, d_hi, *, with_tar=True,
     nbytes = cost_workspace_bytes(B, H, W)
     if workspace is None:
         workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    for t, name in ((vol_ref, "vol_ref"), (vol_tar, "vol_tar")):
+        _expect(t, torch.float32, (B, H, W, D), name)
+    for t, name in ((nan_ref, "nan_ref"), (nan_tar, "nan_tar")):
+        _expect(t, torch.uint8, (B, H, W), name)
+    if workspace.dtype != torch.uint8 or workspace.dim() != 1 or workspace.numel() < nbytes:
+        raise ValueError(f"rsr: workspace must be a uint8 vector of >= {nbytes} bytes")
     check("rsr_cost_volume", lib().rsr_cost_volume(
         s, RsrCostParams(rho_block, d_lo, d_hi), _ptr(ref), _ptr(warped), _ptr(valid), _ptr(vol_ref),
         _ptr(vol_tar), _ptr(nan_ref), _ptr(nan_tar), _ptr(workspace), workspace.numel(), _stream()))
@@ -97,14 +116,28 @@ def rsr_aggregate(vol, guide, rho, gamma_d, gamma_r, nan_map=None, out=None, con
     if vol.dim() == 3:
         vol = vol.unsqueeze(0)
     D = vol.shape[-1]
+    _expect(guide, torch.uint8, (B, H, W), "guide")
     _expect(vol, torch.float32, (B, H, W, D), "vol")
     out = torch.empty_like(vol) if out is None else out
+    _expect(out, torch.float32, (B, H, W, D), "out")
+    if out.data_ptr() == vol.data_ptr():
+        raise ValueError("rsr: out must not alias vol")
     if nan_map is not None:
         nan_map, _ = _bhw(nan_map)
+        _expect(nan_map, torch.uint8, (B, H, W), "nan_map")
     check("rsr_aggregate", lib().rsr_aggregate(
         s, D, RsrAggParams(rho, float(gamma_d), float(gamma_r), int(concurrency)), _ptr(vol), _ptr(guide),
         _ptr(nan_map), _ptr(out), _stream()))
     return out
+
+
+def rsr_aggregate_rows(B, H, W, D, rho, concurrency=1) -> int:
+    """Output rows per CTA rsr_aggregate uses for these arguments (0: the rho > 7 tiled
+    kernel); host-only introspection for tests and tools."""
+    r = int(lib().rsr_aggregate_rows(RsrShape(B, H, W), int(D), RsrAggParams(int(rho), 1.0, 1.0, int(concurrency))))
+    if r < 0:
+        raise ValueError("rsr_aggregate_rows: invalid arguments")
+    return r
 
 
 def rsr_disparity(agg_ref, agg_tar, shift, d_lo, d_hi, lrc_tol, subpixel=True, disparity=None,
@@ -113,6 +146,10 @@ def rsr_disparity(agg_ref, agg_tar, shift, d_lo, d_hi, lrc_tol, subpixel=True, d
     if agg_ref.dim() == 3:
         agg_ref, agg_tar = agg_ref.unsqueeze(0), agg_tar.unsqueeze(0)
     B, H, W, D = agg_ref.shape
+    if D != d_hi - d_lo + 1:
+        raise ValueError(f"rsr: volumes hold D = {D} disparities, range [{d_lo}, {d_hi}] needs {d_hi - d_lo + 1}")
+    _expect(agg_ref, torch.float32, (B, H, W, D), "agg_ref")
+    _expect(agg_tar, torch.float32, (B, H, W, D), "agg_tar")
     shift = shift.reshape(B, H)
     _expect(shift, torch.int32, (B, H), "shift")
     dev = agg_ref.device
@@ -120,6 +157,9 @@ def rsr_disparity(agg_ref, agg_tar, shift, d_lo, d_hi, lrc_tol, subpixel=True, d
     if with_wta:
         wta_ref = torch.empty((B, H, W), dtype=torch.int16, device=dev) if wta_ref is None else wta_ref
         wta_tar = torch.empty((B, H, W), dtype=torch.int16, device=dev) if wta_tar is None else wta_tar
+    _expect(disparity, torch.float32, (B, H, W), "disparity")
+    _expect(wta_ref, torch.int16, (B, H, W), "wta_ref")
+    _expect(wta_tar, torch.int16, (B, H, W), "wta_tar")
     check("rsr_disparity", lib().rsr_disparity(
         RsrShape(B, H, W), RsrDispParams(d_lo, d_hi, lrc_tol, 1 if subpixel else 0), _ptr(agg_ref),
         _ptr(agg_tar), _ptr(shift), _ptr(disparity), _ptr(wta_ref), _ptr(wta_tar), _stream()))
@@ -133,7 +173,9 @@ def rsr_reconstruct(disparity, f, baseline, u0=None, v0=None, d_min=1.0, xyz=Non
     B, H, W = disparity.shape
     u0 = (W - 1) / 2.0 if u0 is None else u0
     v0 = (H - 1) / 2.0 if v0 is None else v0
+    _expect(disparity, torch.float32, (B, H, W), "disparity")
     xyz = torch.empty((B, H, W, 3), dtype=torch.float32, device=disparity.device) if xyz is None else xyz
+    _expect(xyz, torch.float32, (B, H, W, 3), "xyz")
     check("rsr_reconstruct", lib().rsr_reconstruct(
         RsrShape(B, H, W), RsrRig(f, baseline, u0, v0, d_min), _ptr(disparity), _ptr(xyz), _stream()))
     return xyz
@@ -151,9 +193,12 @@ def rsr_road_model(disparity, step_u=4, step_v=4, n_hyp=512, inlier_tol=0.5, see
     p = RsrRoadParams(step_u, step_v, n_hyp, float(inlier_tol), seed & 0xFFFFFFFF)
     dev = disparity.device
     model = torch.empty((B, 3), dtype=torch.float64, device=dev) if model is None else model
+    _expect(model, torch.float64, (B, 3), "model")
     nbytes = int(lib().rsr_road_workspace_size(s, p))
     if workspace is None:
         workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+    if workspace.dtype != torch.uint8 or workspace.dim() != 1 or workspace.numel() < nbytes:
+        raise ValueError(f"rsr: workspace must be a uint8 vector of >= {nbytes} bytes")
     check("rsr_road_model", lib().rsr_road_model(s, p, _ptr(disparity), _ptr(model), _ptr(workspace),
                                                  workspace.numel(), _stream()))
     return model
@@ -167,12 +212,10 @@ def rsr_road_roll(disparity, u0, u1, v0, v1, out=None):
     B, H, W = disparity.shape
     _expect(disparity, torch.float32, (B, H, W), "disparity")
     out = torch.empty((B, 5), dtype=torch.float64, device=disparity.device) if out is None else out
+    _expect(out, torch.float64, (B, 5), "out")
     check("rsr_road_roll", lib().rsr_road_roll(RsrShape(B, H, W), u0, u1, v0, v1, _ptr(disparity), _ptr(out),
                                                _stream()))
     return out
-
-
-_ = math  # (kept for callers that pass math.inf for gamma_r)
 
 
 def rsr_plane_fit(corners, plane=None):
@@ -198,6 +241,7 @@ def rsr_plane_distance(plane, xyz, dist=None):
     _expect(xyz, torch.float32, (B, H, W, 3), "xyz")
     _expect(plane, torch.float64, (B, 4), "plane")
     dist = torch.empty((B, H, W), dtype=torch.float32, device=xyz.device) if dist is None else dist
+    _expect(dist, torch.float32, (B, H, W), "dist")
     check("rsr_plane_distance", lib().rsr_plane_distance(RsrShape(B, H, W), _ptr(plane), _ptr(xyz), _ptr(dist),
                                                          _stream()))
     return dist
@@ -214,6 +258,7 @@ def rsr_search_range(disparity, shift, delta, d_lo_limit, d_hi_limit, out=None):
     shift = shift.reshape(B, H)
     _expect(shift, torch.int32, (B, H), "shift")
     out = torch.empty((B, 2), dtype=torch.int32, device=disparity.device) if out is None else out
+    _expect(out, torch.int32, (B, 2), "out")
     check("rsr_search_range", lib().rsr_search_range(RsrShape(B, H, W), _ptr(disparity), _ptr(shift), int(delta),
                                                      int(d_lo_limit), int(d_hi_limit), _ptr(out), _stream()))
     return out

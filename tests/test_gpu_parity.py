@@ -14,6 +14,7 @@ configuration bench.py times and compare on oracle row bands (the oracle
 computes a band exactly as the full image, tests/test_oracle_pins.py).
 """
 import math
+import zlib
 
 import numpy as np
 import pytest
@@ -187,12 +188,9 @@ def test_parity_config5_frames_batched(rsr):
         compare(gpu, ora, rows, cfg, b=b, label=f"c5[{i}]")
 
 
-def test_parity_bench_launch_configuration(rsr):
-    """The exact launch bench.py times: StereoPipeline over an 8-frame c5 batch (the
-    batch size picks K3's row chunking and grid); sampled row bands of three frames
-    against the oracle, and a bitwise rerun."""
-    cfg = synth.get_config("c5")
-    B = 8
+def pipeline_parity(rsr, cfg, B, picks, bitwise_rerun=False):
+    """Run StereoPipeline (the launch bench.py times) over a B-frame batch of cfg and
+    compare oracle row bands of the picked frames.  picks: [(frame, (r0, r1))]."""
     left, right, ab = synth.make_batch(cfg, list(range(B)))
     L = torch.from_numpy(left).cuda()
     R = torch.from_numpy(right).cuda()
@@ -204,14 +202,59 @@ def test_parity_bench_launch_configuration(rsr):
     gpu = dict(warped=g(pipe.warped), mask=g(pipe.valid), shift=g(pipe.shift), cost_ref=g(pipe.vol_ref),
                cost_tar=g(pipe.vol_tar), agg_ref=g(pipe.agg_ref), agg_tar=g(pipe.agg_tar),
                disparity=g(pipe.disparity), k_ref=g(pipe.wta_ref), k_tar=g(pipe.wta_tar), xyz=g(pipe.xyz))
-    for b, rows in ((0, (0, 6)), (3, (141, 147)), (7, (714, 720))):   # chunk edges of R = 144
+    for b, rows in picks:
         check_warp(gpu, right[b], ab[b], b)
         ora = O.run_pipeline(left[b], right[b], ab[b][0], ab[b][1], cfg, rows=rows)
-        compare(gpu, ora, rows, cfg, b=b, label=f"bench c5[{b}]{rows}")
-    d0 = pipe.disparity.clone()
-    pipe.run(L, R, AB, with_wta=True)
-    torch.cuda.synchronize()
-    assert torch.equal(torch.nan_to_num(d0, nan=-7.0), torch.nan_to_num(pipe.disparity, nan=-7.0))
+        rep = compare(gpu, ora, rows, cfg, b=b, label=f"{cfg.name} D={cfg.D} [{b}]{rows}")
+        print(cfg.name, cfg.D, b, rows, rep)
+    if bitwise_rerun:
+        d0 = pipe.disparity.clone()
+        pipe.run(L, R, AB, with_wta=True)
+        torch.cuda.synchronize()
+        assert torch.equal(torch.nan_to_num(d0, nan=-7.0), torch.nan_to_num(pipe.disparity, nan=-7.0))
+
+
+def chunk_edge_bands(rsr, cfg, B, half=3):
+    """Row bands straddling K3's real row-chunk edges for this launch (R from the
+    library's own plan for the pipeline's concurrency of 2), plus the first and
+    last rows of the image."""
+    R = rsr.rsr_aggregate_rows(B, cfg.height, cfg.width, cfg.D, cfg.rho_agg, concurrency=2)
+    assert 8 <= R < cfg.height, R
+    edges = list(range(R, cfg.height, R))
+    bands = [(0, 2 * half)] + [(e - half, e + half) for e in edges[:2]] + [(cfg.height - 2 * half, cfg.height)]
+    return R, bands
+
+
+def test_parity_bench_launch_configuration(rsr):
+    """The exact launch bench.py times: StereoPipeline over an 8-frame c5 batch (the
+    batch size picks K3's row chunking and grid); row bands straddling the real K3
+    chunk edges (R from rsr_aggregate_rows: 240 at c5 / B = 8 / concurrency 2) of
+    several frames against the oracle, and a bitwise rerun."""
+    cfg = synth.get_config("c5")
+    R, bands = chunk_edge_bands(rsr, cfg, 8)
+    picks = [(b, rows) for b, rows in zip((0, 3, 5, 7), bands)]
+    pipeline_parity(rsr, cfg, 8, picks, bitwise_rerun=True)
+
+
+def test_parity_paper_operating_point_full_size(rsr):
+    """The paper's operating point cP (1240x609, d_max = 30, 7x7 NCC, 9x9
+    bilateral) in the 8-frame launch tools/paper_sweep.py times: the two-CTA
+    small-slab K3 with 8-byte cp.async staging (D = 30 = 2 mod 4) and R sized for
+    H = 609; bands at the real chunk edges."""
+    cfg = synth.get_config("cP")
+    R, bands = chunk_edge_bands(rsr, cfg, 8)
+    picks = [(b, rows) for b, rows in zip((0, 2, 6, 7), bands)]
+    pipeline_parity(rsr, cfg, 8, picks)
+
+
+@pytest.mark.parametrize("d_lo,d_hi", [(-3, 2), (-4, 3), (-6, 5)])
+def test_parity_restricted_band_full_size(rsr, d_lo, d_hi):
+    """Restricted search ranges at c5 size in the 8-frame launch
+    tools/range_bench.py times: D = 6 (8-byte cp.async rows), 8 (compact rows), 12."""
+    cfg = synth.get_config("c5", d_lo=d_lo, d_hi=d_hi)
+    R, bands = chunk_edge_bands(rsr, cfg, 8)
+    picks = [(b, rows) for b, rows in zip((1, 4, 6, 7), bands)]
+    pipeline_parity(rsr, cfg, 8, picks)
 
 
 EDGE_CASES = {
@@ -235,6 +278,10 @@ EDGE_CASES = {
     "D14_rho3": (30, 77, -7, 6, 2, 3, 3.0, 10.0, 0.02, 1.0),
     # largest NCC block (15x15): block statistics need > 48 KB of shared memory
     "rho_block7": (44, 100, -4, 11, 7, 2, 2.0, 10.0, 0.0, 2.0),
+    # rho 8..10: the tiled K3 kernel (aggregate.cu), one and two disparity slabs
+    "rho8_D16": (40, 90, -8, 7, 2, 8, 5.0, 12.0, 0.05, 2.0),
+    "rho9_D70_two_slabs": (38, 84, -35, 34, 2, 9, 5.0, 12.0, 0.0, 1.0),
+    "rho10_D24": (48, 100, -12, 11, 3, 10, 6.0, 12.0, 0.05, 2.0),
 }
 
 
@@ -243,7 +290,7 @@ def test_parity_edge_cases(rsr, case):
     H, W, d_lo, d_hi, rb, ra, gd, gr, a, be = EDGE_CASES[case]
     cfg = synth.get_config("c1", height=H, width=W, d_lo=d_lo, d_hi=d_hi, rho_block=rb,
                            rho_agg=ra, gamma_d=gd, gamma_r=gr)
-    left, right = synth.tiny_pair(hash(case) % 1000, H, W, shift=3)
+    left, right = synth.tiny_pair(zlib.crc32(case.encode()) % 1000, H, W, shift=3)  # stable across processes
     left = left.copy()
     if H > 12 and W > 12:
         left[2:9, 2:9] = 90  # constant patch: sigma = 0 blocks -> NaN costs
