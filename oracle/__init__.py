@@ -6,3 +6,4 @@ with paper_1807_07433_b200/ and imports nothing from it.
 """
 from .rsr_oracle import *  # noqa: F401,F403
 from . import brute  # noqa: F401
+from . import interp_warp  # noqa: F401
