@@ -191,6 +191,38 @@ int rsr_reconstruct(rsr_shape s, rsr_rig rig, const float* disparity,
                     float* xyz, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Interpolating-warp variant (NEXT row f2; reading 21).      */
+/* ("shifted alpha_0 + alpha_1 v - delta pixels") is silent on fractional     */
+/* shifts; the main path rounds them (rsr_warp).  This variant resamples the  */
+/* target row by linear interpolation at x = u - t(v), t = alpha v + beta     */
+/* (fp64), with the position quantised to 1/256 px (q = floor(256 f + 1/2),   */
+/* f = x - floor(x); q = 256 carries), and stores 8.8 fixed point:            */
+/*   warped[b][v][u] = (256 - q) T(x0) + q T(x0 + 1)   (uint16, <= 65280)     */
+/*   valid = 1 iff both samples (one when q = 0) lie in the row, else 0, 0    */
+/*   shift[b][v] = t_q(v) = -(x0(u=0) + q/256), the shift actually applied    */
+/* The NCC (Eqs. 3-5) of (ref, warped) is scale invariant, so the four calls  */
+/* below mirror rsr_cost_volume / rsr_aggregate / rsr_disparity with exact    */
+/* integer sums; the target volume's guide is warped/256 (real intensities);  */
+/* post-processing adds the fp64 t_q(v): d = fp32(r_s + t_q(v)).             */
+/* Arguments, layouts, ownership and errors are those of the integer calls,   */
+/* with: warped uint16 [B][H][W]; shift double [B][H]; rsr_aggregate_linear   */
+/* takes a uint16 guide and rho <= 7 (RSR_E_ARG above); rsr_cost_volume_linear */
+/* needs 2B <= 65535.  The workspace is rsr_cost_workspace_size(s).           */
+int rsr_warp_linear(rsr_shape s, const double* alpha_beta, const uint8_t* target,
+                    uint16_t* warped, uint8_t* valid, double* shift, void* stream);
+int rsr_cost_volume_linear(rsr_shape s, rsr_cost_params p, const uint8_t* ref,
+                           const uint16_t* warped, const uint8_t* valid,
+                           float* vol_ref, float* vol_tar, uint8_t* nan_ref,
+                           uint8_t* nan_tar, void* workspace, size_t workspace_bytes,
+                           void* stream);
+int rsr_aggregate_linear(rsr_shape s, int32_t D, rsr_agg_params p, const float* vol,
+                         const uint16_t* guide, const uint8_t* nan_map, float* out,
+                         void* stream);
+int rsr_disparity_linear(rsr_shape s, rsr_disp_params p, const float* agg_ref,
+                         const float* agg_tar, const double* shift, float* disparity,
+                         int16_t* wta_ref, int16_t* wta_tar, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Road model (before the path: Eq. (2)).  Robust least-squares fit */
 /* of the road's v-disparity line d = alpha * v + beta ("estimated by solving */
 /* a least squares problem with a collection of reliable correspondence      */

@@ -49,6 +49,10 @@ constexpr int SG_NSC = 4;       // cost stages
 constexpr int SG_NSW = 3;       // weight stages
 constexpr int SG_SEGMAX = 720;  // max output rows per segment (guide tile height)
 constexpr short SG_GSKIP = 600;     // integer guide tile: skipped pixel (outside / all-NaN)
+// skip code of the guide tile: 600 for uint8 guides (indexes the zero tail of the range
+// table), 0xFFFF for 8.8 fixed-point guides (NEXT f2: values <= 65280)
+template <bool G16>
+RSR_DEVINL int gskip() { return G16 ? 0xFFFF : SG_GSKIP; }
 constexpr int SG_RLUT = 2 * 600 + 255 + 1;   // range table, zero beyond |dg| = 255
 
 struct SlideGeom {
@@ -117,7 +121,7 @@ struct SlideArgs {
   int nstrips;           // 32-column strips
   float kd, kr;
   const float* vol;
-  const uint8_t* guide;
+  const void* guide;     // uint8 [B][H][W], or uint16 8.8 fixed point (G16)
   const uint8_t* nan_map;
   float* out;
 };
@@ -158,9 +162,9 @@ __host__ __device__ inline bool stage_cpasync(int D, const SlideGeom& g) {
   return (D & 3) == 2 && (g.KS & (g.KS - 1)) == 0;
 }
 
-template <int RHO>
+template <int RHO, bool G16>
 __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g, const Seg& s, bool clean,
-                                          int i, const short* gt, float* cost_s, uint64_t* full_c, uint64_t* empty_c,
+                                          int i, const unsigned short* gt, float* cost_s, uint64_t* full_c, uint64_t* empty_c,
                                           uint32_t& it_c, int lane, int t = 0, int nt = 32) {
   const bool bulk = (A.D & 3) == 0;
   const float fillv = clean ? 0.f : qnan();
@@ -177,7 +181,7 @@ __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g
       const int col = e >> lg, k = 2 * (e & ((1 << lg) - 1));
       float* d = dst + col * g.KS + k;
       // the guide tile marks outside and all-NaN pixels: filled, not copied
-      const bool skip = !row_in || gt[(i + RHO) * g.CX + col] == SG_GSKIP;
+      const bool skip = !row_in || gt[(i + RHO) * g.CX + col] == gskip<G16>();
       if (!skip && k < s.ks_eff) {
         cp_async8(d, A.vol + (rowpix + (s.x0 - RHO + col)) * A.D + s.k0 + k);
       } else {
@@ -198,7 +202,7 @@ __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g
     // the guide tile marks outside and all-NaN pixels (+inf): fill them instead of copying
     // (all-NaN -> 0 on a clean segment, where such taps carry weight 0; NaN otherwise)
     const bool skip = !(col < g.CX && row_in) ||
-                      gt[(i + RHO) * g.CX + col] == SG_GSKIP;
+                      gt[(i + RHO) * g.CX + col] == gskip<G16>();
     cp[h] = !skip && bulk;
     if (col < g.CX) {
       float* d = dst + col * g.CS;
@@ -244,9 +248,9 @@ __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g
 // FFMA2 accumulates its per-disparity denominators: both paths give bitwise
 // identical results wherever both apply, whatever the segmentation (batch-size
 // independence).  Warp 0 also stages the cost rows.
-template <int RHO>
+template <int RHO, bool G16>
 __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideGeom& g, const Seg& s,
-                                                bool clean, int npass, const short* gt, float* w_s,
+                                                bool clean, int npass, const unsigned short* gt, float* w_s,
                                                 float* dsum, float* cost_s, uint64_t* full_w,
                                                 uint64_t* empty_w, uint64_t* full_c, uint64_t* empty_c,
                                                 uint32_t& it_w, uint32_t& it_c, int p, int lane,
@@ -270,7 +274,7 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
     for (int i = 0; i < NR; i++, it_w++) {
       // cp.async-staged rows: every producer warp issues a share (non-blocking)
       if (cpa || p == 0)
-        stage_row<RHO>(A, g, s, clean, i, gt, cost_s, full_c, empty_c, it_c, lane, p * 32 + lane, SG_NPROD * 32);
+        stage_row<RHO, G16>(A, g, s, clean, i, gt, cost_s, full_c, empty_c, it_c, lane, p * 32 + lane, SG_NPROD * 32);
       const int st = it_w % SG_NSW;
       if (it_w >= SG_NSW) mbar_wait_parity(&empty_w[st], ((it_w / SG_NSW) & 1) ^ 1);
       float* wst = w_s + (size_t)st * g.WST;
@@ -282,19 +286,31 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
       // w = S(a, j) * R(g(q) - g(p)): spatial factor per (age, tap) held in registers
       // for the whole kernel (sreg), range factor from a shared table indexed by the
       // integer guide difference (skipped pixels index the zero tail of the table).
-      const short* trs = gt + (i + RHO) * g.CX;   // tap row r
+      const unsigned short* trs = gt + (i + RHO) * g.CX;   // tap row r
 #pragma unroll
       for (int n = 0; n < NAB; n++) {
         const int item = p + 4 * n;
         const int x = (item / NAB) * 8 + xs, a = (item % NAB) * 4 + as;
         const int ac = min(a, NT - 1);
         int gp = gt[(i + ac) * g.CX + x + RHO];
-        gp = (gp == SG_GSKIP) ? -SG_GSKIP : gp;
         float* slot = dsum + ((i + ac) % NT) * 32 + x;
         float d = *slot;
         float w[NT];
+        if (G16) {
+          // 8.8 fixed-point guide: range factor exp2(kr (dg / 256)^2) on the MUFU pipe,
+          // zero for skipped pixels (the tap's or the centre's)
+          const bool pskip = gp == gskip<G16>();
 #pragma unroll
-        for (int j = 0; j < NT; j++) w[j] = sreg[n][j] * rlut[trs[x + j] - gp + 255];
+          for (int j = 0; j < NT; j++) {
+            const int gq = trs[x + j];
+            const float dg = (float)(gq - gp);
+            w[j] = (pskip || gq == gskip<G16>()) ? 0.f : sreg[n][j] * ex2_ftz(A.kr * (dg * dg));
+          }
+        } else {
+          gp = (gp == SG_GSKIP) ? -SG_GSKIP : gp;
+#pragma unroll
+          for (int j = 0; j < NT; j++) w[j] = sreg[n][j] * rlut[trs[x + j] - gp + 255];
+        }
         if (a < NT) {
           float* wd = wst + x * g.XS + a;
 #pragma unroll
@@ -383,11 +399,11 @@ RSR_DEVINL void slide_row(float2 (&acc)[2 * RHO + 1][4], float2 (&fin)[4], const
 }
 
 // ---- consumers (G warps): sliding accumulation, FFMA2 -----------------------
-template <int RHO, bool CLEAN>
+template <int RHO, bool CLEAN, bool G16>
 __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, const Seg& s,
                                         const float* cost_s, const float* w_s, uint64_t* full_c,
                                         uint64_t* empty_c, uint64_t* full_w, uint64_t* empty_w,
-                                        uint32_t& it, int xl, int l, int lane, const short* gt,
+                                        uint32_t& it, int xl, int l, int lane, const unsigned short* gt,
                                         int hcmask) {
   constexpr int NT = 2 * RHO + 1;
   constexpr int NPASS = CLEAN ? 1 : 2;
@@ -397,7 +413,7 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
   // A warp whose output pixels are all skipped (centre outside the image or all-NaN)
   // writes NaN and only keeps the pipeline hand-off going: no FFMA2.
   bool live = false;
-  for (int y = s.ya + l; y < s.yb; y += g.G) live |= gt[(y - s.ya + 2 * RHO) * g.CX + xl + RHO] != SG_GSKIP;
+  for (int y = s.ya + l; y < s.yb; y += g.G) live |= gt[(y - s.ya + 2 * RHO) * g.CX + xl + RHO] != gskip<G16>();
   if (!__any_sync(0xffffffffu, live)) {
     for (int pass = 0; pass < NPASS; pass++) {
       const int koff = CLEAN ? 4 * l : 4 * g.G * pass + 4 * l;
@@ -503,7 +519,7 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
 // MINB = 1: up to 8 consumer warps (D up to 64 per slab), one CTA per SM.  MINB = 2:
 // small slabs (G <= 2 at any rho, G <= 4 at rho <= 5), two CTAs per SM so the few
 // consumer warps of a CTA do not leave the SM idle; the guide tile is sized by R.
-template <int RHO, int MINB, bool COMPACT>
+template <int RHO, int MINB, bool COMPACT, bool G16>
 __global__ void __launch_bounds__(MINB == 1 ? 384 : (RHO <= 5 ? 256 : 192), MINB)
     k_aggregate_slide(const SlideArgs A) {
   extern __shared__ __align__(128) unsigned char sl_smem[];
@@ -511,7 +527,7 @@ __global__ void __launch_bounds__(MINB == 1 ? 384 : (RHO <= 5 ? 256 : 192), MINB
   float* cost_s = reinterpret_cast<float*>(sl_smem + g.off_cost);
   float* w_s = reinterpret_cast<float*>(sl_smem + g.off_w);
   float* dpart = reinterpret_cast<float*>(sl_smem + g.off_dpart);
-  short* gt = reinterpret_cast<short*>(sl_smem + g.off_guide);
+  unsigned short* gt = reinterpret_cast<unsigned short*>(sl_smem + g.off_guide);
   float* rlut = reinterpret_cast<float*>(sl_smem + g.off_rlut);
   // range factor exp2(kr dg^2) at index dg + 255; zero for the skip encodings
   for (int t = threadIdx.x; t < SG_RLUT; t += blockDim.x) {
@@ -548,7 +564,8 @@ __global__ void __launch_bounds__(MINB == 1 ? 384 : (RHO <= 5 ? 256 : 192), MINB
     const int rows = (s.yb - s.ya) + 4 * RHO;
     constexpr int UNR = 8;   // independent loads in flight per thread
     for (int e0 = tid; e0 < rows * g.CX; e0 += UNR * blockDim.x) {
-      uint8_t mv[UNR], gv[UNR];
+      uint8_t mv[UNR];
+    unsigned short gv[UNR];
 #pragma unroll
       for (int u = 0; u < UNR; u++) {
         const int e = e0 + u * blockDim.x;
@@ -558,7 +575,8 @@ __global__ void __launch_bounds__(MINB == 1 ? 384 : (RHO <= 5 ? 256 : 192), MINB
         if (e < rows * g.CX && yy >= 0 && yy < A.H && xx >= 0 && xx < A.W) {
           const size_t pi = s.pix0 + (size_t)yy * A.W + xx;
           mv[u] = A.nan_map ? __ldg(A.nan_map + pi) : 2;
-          gv[u] = __ldg(A.guide + pi);
+          gv[u] = G16 ? __ldg(static_cast<const uint16_t*>(A.guide) + pi)
+                      : (unsigned short)__ldg(static_cast<const uint8_t*>(A.guide) + pi);
         }
       }
 #pragma unroll
@@ -573,7 +591,7 @@ __global__ void __launch_bounds__(MINB == 1 ? 384 : (RHO <= 5 ? 256 : 192), MINB
             dirty |= ((mv[u] & 0x80) && g.nslab == 1) ? ((mv[u] >> 2) & 3) : 3;
           }
           // +inf marks a skipped pixel (outside the image or all-NaN)
-          gt[e] = (mv[u] & 3) == 1 ? SG_GSKIP : (short)gv[u];
+          gt[e] = (mv[u] & 3) == 1 ? (unsigned short)gskip<G16>() : gv[u];
         }
       }
     }
@@ -582,14 +600,14 @@ __global__ void __launch_bounds__(MINB == 1 ? 384 : (RHO <= 5 ? 256 : 192), MINB
     const int hcmask = (__syncthreads_or(dirty & 1) ? 0 : 1) | (__syncthreads_or(dirty & 2) ? 0 : 2);
     const int npass = clean ? 1 : 2;
     if (warp >= n_cons) {
-      produce_weights<RHO>(A, g, s, clean, npass, gt, w_s, dpart, cost_s, full_w, empty_w, full_c, empty_c,
+      produce_weights<RHO, G16>(A, g, s, clean, npass, gt, w_s, dpart, cost_s, full_w, empty_w, full_c, empty_c,
                            it, it_c, warp - n_cons, lane, rlut);
     } else {
       const int t = tid;   // consumer thread: column t / G, lane-in-group t % G
       if (clean)
-        consume<RHO, true>(A, g, s, cost_s, w_s, full_c, empty_c, full_w, empty_w, it, t / g.G, t % g.G, lane, gt, hcmask);
+        consume<RHO, true, G16>(A, g, s, cost_s, w_s, full_c, empty_c, full_w, empty_w, it, t / g.G, t % g.G, lane, gt, hcmask);
       else
-        consume<RHO, false>(A, g, s, cost_s, w_s, full_c, empty_c, full_w, empty_w, it, t / g.G, t % g.G, lane, gt, hcmask);
+        consume<RHO, false, G16>(A, g, s, cost_s, w_s, full_c, empty_c, full_w, empty_w, it, t / g.G, t % g.G, lane, gt, hcmask);
     }
   }
 }
@@ -647,14 +665,16 @@ static SlidePlan slide_plan(int B, int H, int W, int D, int rho, int conc, int n
   return p;
 }
 
+#ifndef RSR_SLIDE_G16
 int aggregate_plan_rows(int B, int H, int W, int D, int rho, int conc) {
   if (rho > 7) return 0;   // tiled kernel (aggregate.cu): no row chunks
   return slide_plan(B, H, W, D, rho, conc, sm_count()).R;
 }
+#endif
 
-template <int RHO>
+template <int RHO, bool G16>
 static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, float gamma_r, int conc,
-                                  const float* vol, const uint8_t* guide, const uint8_t* nan_map,
+                                  const float* vol, const void* guide, const uint8_t* nan_map,
                                   float* out, cudaStream_t st) {
   const SlideGeom g1 = slide_geom(D, RHO);
   const SlidePlan plan = slide_plan(B, H, W, D, RHO, conc, sm_count());
@@ -667,24 +687,36 @@ static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, flo
   const float log2e = 1.4426950408889634f;
   A.kd = -log2e / (gamma_d * gamma_d);
   A.kr = std::isinf(gamma_r) ? -1e-30f : -log2e / (gamma_r * gamma_r);
+  if (G16) A.kr = std::isinf(gamma_r) ? 0.f : A.kr * (1.f / 65536.f);   // guide differences in 1/256 units
   A.vol = vol; A.guide = guide; A.nan_map = nan_map; A.out = out;
   const long long nblk = cols * ((H + plan.R - 1) / plan.R);
   if (nblk > 0x7fffffffLL) return cudaErrorInvalidValue;
-  auto kern = plan.minb == 1 ? k_aggregate_slide<RHO, 1, false>
-                             : (plan.compact ? k_aggregate_slide<RHO, 2, true> : k_aggregate_slide<RHO, 2, false>);
+  auto kern = plan.minb == 1 ? k_aggregate_slide<RHO, 1, false, G16>
+                             : (plan.compact ? k_aggregate_slide<RHO, 2, true, G16>
+                                             : k_aggregate_slide<RHO, 2, false, G16>);
   cudaError_t e = smem_optin((const void*)kern, plan.bytes);
   if (e != cudaSuccess) return e;
   kern<<<(unsigned)nblk, 32 * (g1.G + SG_NPROD), plan.bytes, st>>>(A);
   return cudaGetLastError();
 }
 
+#ifndef RSR_SLIDE_G16
 size_t aggregate_slide_smem(int D, int rho, int H) { (void)H; return slide_geom(D, rho).bytes; }
+#endif
 
+#ifndef RSR_SLIDE_G16
 cudaError_t launch_aggregate_slide(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r, int conc,
                                    const float* vol, const uint8_t* guide, const uint8_t* nan_map,
                                    float* out, cudaStream_t st) {
+  constexpr bool G16 = false;
+#else
+cudaError_t launch_aggregate_slide16(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r, int conc,
+                                     const float* vol, const uint16_t* guide, const uint8_t* nan_map,
+                                     float* out, cudaStream_t st) {
+  constexpr bool G16 = true;
+#endif
 #define RSR_S(R) \
-  case R: return slide_launch_t<R>(B, H, W, D, gamma_d, gamma_r, conc, vol, guide, nan_map, out, st);
+  case R: return slide_launch_t<R, G16>(B, H, W, D, gamma_d, gamma_r, conc, vol, guide, nan_map, out, st);
   switch (rho) {
     RSR_S(0) RSR_S(1) RSR_S(2) RSR_S(3) RSR_S(4) RSR_S(5) RSR_S(6) RSR_S(7)
     default:

@@ -124,6 +124,69 @@ int rsr_disparity(rsr_shape s, rsr_disp_params p, const float* agg_ref, const fl
                                         wta_ref, wta_tar, as_stream(stream)));
 }
 
+// ---- interpolating-warp variant (NEXT row f2, reading 21) ----
+int rsr_warp_linear(rsr_shape s, const double* alpha_beta, const uint8_t* target, uint16_t* warped,
+                    uint8_t* valid, double* shift, void* stream) {
+  if (!shape_ok(s) || !alpha_beta || !target || !warped || !valid || !shift) return RSR_E_ARG;
+  if (s.height > 65535 || s.batch > 65535) return RSR_E_ARG;
+  return launched(rsr::launch_warp_linear(s.batch, s.height, s.width, alpha_beta, target, warped, valid,
+                                          shift, as_stream(stream)));
+}
+
+int rsr_cost_volume_linear(rsr_shape s, rsr_cost_params p, const uint8_t* ref, const uint16_t* warped,
+                           const uint8_t* valid, float* vol_ref, float* vol_tar, uint8_t* nan_ref,
+                           uint8_t* nan_tar, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!shape_ok(s) || !ref || !warped || !valid || !vol_ref || !workspace) return RSR_E_ARG;
+  if (p.rho_block < 1 || p.rho_block > 7 || p.d_hi < p.d_lo) return RSR_E_ARG;
+  const long long D = (long long)p.d_hi - p.d_lo + 1;
+  if (D > 32767) return RSR_E_ARG;
+  if (workspace_bytes < rsr_cost_workspace_size(s)) return RSR_E_ARG;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return RSR_E_ARG;
+  if (s.height < 2 * p.rho_block + 1 || s.width < 2 * p.rho_block + 1) return RSR_E_DATA;
+  if ((size_t)(s.height + 15) / 16 > 65535 || 2LL * s.batch > 65535) return RSR_E_ARG;
+  const size_t chunk = align16(sizeof(int32_t) * npix(s));
+  char* ws = static_cast<char*>(workspace);
+  int32_t* SL = reinterpret_cast<int32_t*>(ws);
+  float* iL = reinterpret_cast<float*>(ws + chunk);
+  int32_t* SW = reinterpret_cast<int32_t*>(ws + 2 * chunk);
+  float* iW = reinterpret_cast<float*>(ws + 3 * chunk);
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = rsr::launch_block_stats16(s.batch, s.height, s.width, p.rho_block, ref, SL, iL, warped, valid,
+                                            SW, iW, st);
+  if (e == cudaSuccess)
+    e = rsr::launch_zncc_fx(s.batch, s.height, s.width, p.rho_block, p.d_lo, (int)D, ref, warped, SL, iL, SW,
+                            iW, vol_ref, vol_tar, st);
+  if (e == cudaSuccess)
+    e = rsr::launch_nan_maps(s.batch, s.height, s.width, p.d_lo, (int)D, iL, iW, nan_ref,
+                             vol_tar ? nan_tar : nullptr, st);
+  return launched(e);
+}
+
+int rsr_aggregate_linear(rsr_shape s, int32_t D, rsr_agg_params p, const float* vol, const uint16_t* guide,
+                         const uint8_t* nan_map, float* out, void* stream) {
+  if (!shape_ok(s) || !vol || !guide || !out) return RSR_E_ARG;
+  if (D < 1 || D > 32767 || p.rho < 0 || p.rho > 7) return RSR_E_ARG;
+  if (!(p.gamma_d > 0.f) || std::isinf(p.gamma_d) || !(p.gamma_r > 0.f)) return RSR_E_ARG;
+  if (p.concurrency < 0 || p.concurrency > 64) return RSR_E_ARG;
+  if (vol == out) return RSR_E_ARG;
+  const long long nslab = (D + 63) / 64;
+  if ((long long)s.batch * nslab > 65535) return RSR_E_ARG;
+  return launched(rsr::launch_aggregate_slide16(s.batch, s.height, s.width, D, p.rho, p.gamma_d, p.gamma_r,
+                                                p.concurrency, vol, guide, nan_map, out, as_stream(stream)));
+}
+
+int rsr_disparity_linear(rsr_shape s, rsr_disp_params p, const float* agg_ref, const float* agg_tar,
+                         const double* shift, float* disparity, int16_t* wta_ref, int16_t* wta_tar,
+                         void* stream) {
+  if (!shape_ok(s) || !agg_ref || !agg_tar || !shift || !disparity) return RSR_E_ARG;
+  if (p.d_hi < p.d_lo || (long long)p.d_hi - p.d_lo + 1 > 32767 || p.lrc_tol < 0) return RSR_E_ARG;
+  if (s.width > 32768 || s.height > 65535 || s.batch > 65535) return RSR_E_ARG;
+  const int D = p.d_hi - p.d_lo + 1;
+  return launched(rsr::launch_disparity_frac(s.batch, s.height, s.width, p.d_lo, D, p.lrc_tol,
+                                             p.subpixel != 0, agg_ref, agg_tar, shift, disparity,
+                                             wta_ref, wta_tar, as_stream(stream)));
+}
+
 size_t rsr_road_workspace_size(rsr_shape s, rsr_road_params p) {
   if (!shape_ok(s) || p.step_u < 1 || p.step_v < 1 || p.n_hyp < 1) return 0;
   return rsr::road_workspace_size(s.batch, s.height, s.width, p.step_u, p.step_v, p.n_hyp);

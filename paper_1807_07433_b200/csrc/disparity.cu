@@ -73,10 +73,13 @@ RSR_DEVINL int group_argmax(const float* __restrict__ p, int D, int l, bool vec4
   return group_reduce(best, kb);
 }
 
+// ShiftT: int32_t (integer warp, reading 1: d = r_s + s(v) in fp32) or double (the
+// interpolating warp, reading 21: d = fp32(r_s + t_q(v)) with the sum in fp64).
+template <typename ShiftT>
 __global__ void __launch_bounds__(256) k_disparity(int H, int W, int d_lo, int D, int tol,
                                                    int subpix, const float* __restrict__ agg_ref,
                                                    const float* __restrict__ agg_tar,
-                                                   const int32_t* __restrict__ shift,
+                                                   const ShiftT* __restrict__ shift,
                                                    float* __restrict__ disp,
                                                    int16_t* __restrict__ wta_ref,
                                                    int16_t* __restrict__ wta_tar) {
@@ -108,7 +111,7 @@ __global__ void __launch_bounds__(256) k_disparity(int H, int W, int d_lo, int D
     }
   }
   __syncthreads();
-  const float sv = (float)shift[(size_t)b * H + v];
+  const ShiftT sv = shift[(size_t)b * H + v];
   for (int u0 = g; u0 < Wr; u0 += UP * ng) {
     float bv[UP];
     int bk[UP];
@@ -136,7 +139,7 @@ __global__ void __launch_bounds__(256) k_disparity(int H, int W, int d_lo, int D
               const float den = 2.f * a + 2.f * c - 4.f * bb;
               if (!(a != a) && !(c != c) && fabsf(den) > 1e-12f) r += __fdiv_rn(a - c, den);
             }
-            d = r + sv;
+            d = sizeof(ShiftT) == 4 ? r + (float)sv : (float)((double)r + (double)sv);
           }
         }
       }
@@ -149,11 +152,23 @@ cudaError_t launch_disparity(int B, int H, int W, int d_lo, int D, int tol, int 
                              const float* agg_ref, const float* agg_tar, const int32_t* shift,
                              float* disp, int16_t* wta_ref, int16_t* wta_tar, cudaStream_t st) {
   const size_t smem = sizeof(int16_t) * (size_t)W;
-  const cudaError_t e = smem_optin((const void*)k_disparity, smem);
+  const cudaError_t e = smem_optin((const void*)k_disparity<int32_t>, smem);
   if (e != cudaSuccess) return e;
   dim3 grid(H, B);
-  k_disparity<<<grid, 256, smem, st>>>(H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, shift, disp,
-                                       wta_ref, wta_tar);
+  k_disparity<int32_t><<<grid, 256, smem, st>>>(H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, shift, disp,
+                                                wta_ref, wta_tar);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_disparity_frac(int B, int H, int W, int d_lo, int D, int tol, int subpix,
+                                  const float* agg_ref, const float* agg_tar, const double* shift,
+                                  float* disp, int16_t* wta_ref, int16_t* wta_tar, cudaStream_t st) {
+  const size_t smem = sizeof(int16_t) * (size_t)W;
+  const cudaError_t e = smem_optin((const void*)k_disparity<double>, smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(H, B);
+  k_disparity<double><<<grid, 256, smem, st>>>(H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, shift, disp,
+                                               wta_ref, wta_tar);
   return cudaGetLastError();
 }
 

@@ -9,6 +9,9 @@ namespace rsr {
 
 cudaError_t launch_warp(int B, int H, int W, const double* ab, const uint8_t* target,
                         uint8_t* warped, uint8_t* valid, int32_t* shift, cudaStream_t st);
+// interpolating warp (NEXT f2): 8.8 fixed-point warped image, fp64 applied shift t_q(v)
+cudaError_t launch_warp_linear(int B, int H, int W, const double* ab, const uint8_t* target,
+                               uint16_t* warped, uint8_t* valid, double* shift, cudaStream_t st);
 
 // Per-pixel block statistics for the NCC normalisation: S = sum i (int32),
 // inv = 1/sqrt(n*sum i^2 - S^2) (fp32, NaN if the block leaves the image, touches
@@ -28,6 +31,16 @@ cudaError_t launch_zncc(bool tar, int B, int H, int W, int rho_b, int d_lo, int 
                         const float* invL, const int32_t* SW, const float* invW, float* vol,
                         cudaStream_t st);
 
+// block statistics with an 8.8 fixed-point second image (NEXT f2)
+cudaError_t launch_block_stats16(int B, int H, int W, int rho_b, const uint8_t* img0, int32_t* S0, float* inv0,
+                                 const uint16_t* img1, const uint8_t* mask1, int32_t* S1, float* inv1,
+                                 cudaStream_t st);
+// NCC volumes of (uint8 ref, 8.8 fixed-point warped), exact integer sums (zncc_fx.cu);
+// vol_tar may be null
+cudaError_t launch_zncc_fx(int B, int H, int W, int rho_b, int d_lo, int D, const uint8_t* ref,
+                           const uint16_t* warped, const int32_t* SL, const float* iL, const int32_t* SW,
+                           const float* iW, float* vol_ref, float* vol_tar, cudaStream_t st);
+
 // Per-pixel NaN summaries of both volumes, from the block norms (either map optional).
 cudaError_t launch_nan_maps(int B, int H, int W, int d_lo, int D, const float* invL,
                             const float* invW, uint8_t* nan_ref, uint8_t* nan_tar, cudaStream_t st);
@@ -41,6 +54,10 @@ cudaError_t launch_aggregate_slide(int B, int H, int W, int D, int rho, float ga
                                    float gamma_r, int conc, const float* vol, const uint8_t* guide,
                                    const uint8_t* nan_map, float* out, cudaStream_t st);
 size_t aggregate_slide_smem(int D, int rho, int H);
+// the same with an 8.8 fixed-point (uint16) guide (interpolating warp, NEXT f2); rho <= 7
+cudaError_t launch_aggregate_slide16(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r, int conc,
+                                     const float* vol, const uint16_t* guide, const uint8_t* nan_map,
+                                     float* out, cudaStream_t st);
 // output rows per CTA the sliding kernel uses for this call (0: tiled kernel, rho > 7)
 int aggregate_plan_rows(int B, int H, int W, int D, int rho, int conc);
 size_t aggregate_tiled_smem(int D, int rho);
@@ -48,6 +65,10 @@ size_t aggregate_tiled_smem(int D, int rho);
 cudaError_t launch_disparity(int B, int H, int W, int d_lo, int D, int tol, int subpix,
                              const float* agg_ref, const float* agg_tar, const int32_t* shift,
                              float* disp, int16_t* wta_ref, int16_t* wta_tar, cudaStream_t st);
+
+cudaError_t launch_disparity_frac(int B, int H, int W, int d_lo, int D, int tol, int subpix,
+                                  const float* agg_ref, const float* agg_tar, const double* shift,
+                                  float* disp, int16_t* wta_ref, int16_t* wta_tar, cudaStream_t st);
 
 cudaError_t launch_reconstruct(int B, int H, int W, double f, double baseline, double u0,
                                double v0, double d_min, const float* disp, float* xyz,

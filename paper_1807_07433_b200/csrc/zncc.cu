@@ -19,6 +19,7 @@
 // Output layout [B][H][W][D]: the thread's 8 disparities of one pixel are 32
 // contiguous bytes (two 16-byte stores); 8 lanes cover one pixel's 64 k.
 #include <cstdio>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -34,26 +35,29 @@ namespace rsr {
 constexpr int ST_TX = 64, ST_TY = 32;   // 32 rows: 47 KB of shared memory at p = 3 (< 48 KB)
 
 // Both images in one grid: frames [0, B) are img0 (mask0, S0, inv0), [B, 2B) img1.
-template <int p>
+// img0 is uint8 (the reference image); img1 is uint8 or, for the interpolating
+// warp (NEXT f2), the 8.8 fixed-point warped image (uint16): sums of squares then
+// need int64 (225 * 65280^2 > 2^31).
+template <int p, typename T1>
 __global__ void __launch_bounds__(256) k_block_stats(int B, int H, int W,
                                                      const uint8_t* __restrict__ img0,
                                                      const uint8_t* __restrict__ mask0,
                                                      int32_t* __restrict__ S0, float* __restrict__ inv0,
-                                                     const uint8_t* __restrict__ img1,
+                                                     const T1* __restrict__ img1,
                                                      const uint8_t* __restrict__ mask1,
                                                      int32_t* __restrict__ S1, float* __restrict__ inv1) {
+  using SST = typename std::conditional<sizeof(T1) == 1, int, long long>::type;
   const bool second = (int)blockIdx.z >= B;
-  const uint8_t* __restrict__ img = second ? img1 : img0;
   const uint8_t* __restrict__ mask = second ? mask1 : mask0;
   int32_t* __restrict__ Sout = second ? S1 : S0;
   float* __restrict__ inv = second ? inv1 : inv0;
-  extern __shared__ int st_smem[];
+  extern __shared__ __align__(16) unsigned char st_raw[];
   const int TC = ST_TX + 2 * p, TR = ST_TY + 2 * p;
-  int* pix = st_smem;                // [TR][TC] value
+  SST* cSS = reinterpret_cast<SST*>(st_raw);         // [ST_TY][TC] vertical sums of squares
+  int* pix = reinterpret_cast<int*>(cSS + ST_TY * TC);  // [TR][TC] value
   int* msk = pix + TR * TC;          // [TR][TC] mask (1 inside image and valid)
   int* cS = msk + TR * TC;           // [ST_TY][TC] vertical sums
-  int* cSS = cS + ST_TY * TC;
-  int* cM = cSS + ST_TY * TC;
+  int* cM = cS + ST_TY * TC;
   const int b = second ? (int)blockIdx.z - B : (int)blockIdx.z, x0 = blockIdx.x * ST_TX, y0 = blockIdx.y * ST_TY;
   const size_t base = (size_t)b * H * W;
   constexpr int UNR = 8;   // independent loads in flight per thread
@@ -65,7 +69,7 @@ __global__ void __launch_bounds__(256) k_block_stats(int B, int H, int W,
       const int yy = y0 - p + i / TC, xx = x0 - p + i % TC;
       const bool in = i < TR * TC && yy >= 0 && yy < H && xx >= 0 && xx < W;
       const size_t g = base + (size_t)yy * W + xx;
-      pv[u] = in ? (int)__ldg(img + g) : 0;
+      pv[u] = in ? (second ? (int)__ldg(img1 + g) : (int)__ldg(img0 + g)) : 0;
       mv[u] = in ? (mask ? (int)(__ldg(mask + g) != 0) : 1) : 0;
     }
 #pragma unroll
@@ -79,11 +83,12 @@ __global__ void __launch_bounds__(256) k_block_stats(int B, int H, int W,
   constexpr int K = 2 * p + 1;
   for (int it = threadIdx.x; it < ST_TY * TC; it += blockDim.x) {
     const int y = it / TC, c = it % TC;
-    int s = 0, ss = 0, m = 0;
+    int s = 0, m = 0;
+    SST ss = 0;
 #pragma unroll
     for (int r = 0; r < K; r++) {
       const int v = pix[(y + r) * TC + c];
-      s += v; ss += v * v; m += msk[(y + r) * TC + c];
+      s += v; ss += (SST)v * v; m += msk[(y + r) * TC + c];
     }
     cS[it] = s; cSS[it] = ss; cM[it] = m;
   }
@@ -94,14 +99,16 @@ __global__ void __launch_bounds__(256) k_block_stats(int B, int H, int W,
     const int y = it / ST_TX, x = it % ST_TX;
     const int yy = y0 + y, xx = x0 + x;
     if (yy >= H || xx >= W) continue;
-    int s = 0, ss = 0, m = 0;
+    int s = 0, m = 0;
+    long long ss = 0;
 #pragma unroll
     for (int d = 0; d < K; d++) {
       s += cS[y * TC + x + d]; ss += cSS[y * TC + x + d]; m += cM[y * TC + x + d];
     }
     const bool inside = yy >= p && yy <= H - 1 - p && xx >= p && xx <= W - 1 - p;
-    // exact integer variance (int64: n * sum(i^2) reaches 3.3e9 at p = 7); its fp32
-    // rounding and MUFU.RSQ stay ~1e-7 relative, far inside the ZNCC tolerance
+    // exact integer variance (int64: n * sum(i^2) reaches 3.3e9 at p = 7 for uint8 and
+    // 2.2e14 for 8.8 fixed point); its fp32 rounding and MUFU.RSQ stay ~1e-7
+    // relative, far inside the ZNCC tolerance
     const long long var = (long long)n * ss - (long long)s * s;
     const bool ok = inside && m == n && var != 0;
     const size_t g = base + (size_t)yy * W + xx;
@@ -110,21 +117,23 @@ __global__ void __launch_bounds__(256) k_block_stats(int B, int H, int W,
   }
 }
 
-cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* img0, const uint8_t* mask0,
-                               int32_t* S0, float* inv0, const uint8_t* img1, const uint8_t* mask1, int32_t* S1,
-                               float* inv1, cudaStream_t st) {
+template <typename T1>
+static cudaError_t block_stats_t(int B, int H, int W, int rho_b, const uint8_t* img0, const uint8_t* mask0,
+                                 int32_t* S0, float* inv0, const T1* img1, const uint8_t* mask1, int32_t* S1,
+                                 float* inv1, cudaStream_t st) {
+  using SST = typename std::conditional<sizeof(T1) == 1, int, long long>::type;
   const int p = rho_b;
   const int TC = ST_TX + 2 * p, TR = ST_TY + 2 * p;
-  const size_t smem = sizeof(int) * (size_t)(2 * TR * TC + 3 * ST_TY * TC);
+  const size_t smem = sizeof(int) * (size_t)(2 * TR * TC + 2 * ST_TY * TC) + sizeof(SST) * (size_t)ST_TY * TC;
   const int nimg = img1 ? 2 : 1;
   if ((long long)nimg * B > 65535) return cudaErrorInvalidValue;
   dim3 grid((W + ST_TX - 1) / ST_TX, (H + ST_TY - 1) / ST_TY, nimg * B);
   switch (p) {
 #define RSR_BS(PP)                                                                              \
   case PP: {                                                                                    \
-    const cudaError_t e = smem_optin((const void*)k_block_stats<PP>, smem);                    \
+    const cudaError_t e = smem_optin((const void*)k_block_stats<PP, T1>, smem);                \
     if (e != cudaSuccess) return e;                                                             \
-    k_block_stats<PP><<<grid, 256, smem, st>>>(B, H, W, img0, mask0, S0, inv0, img1, mask1, S1, inv1); \
+    k_block_stats<PP, T1><<<grid, 256, smem, st>>>(B, H, W, img0, mask0, S0, inv0, img1, mask1, S1, inv1); \
     break;                                                                                      \
   }
     RSR_BS(1) RSR_BS(2) RSR_BS(3) RSR_BS(4) RSR_BS(5) RSR_BS(6) RSR_BS(7)
@@ -132,6 +141,18 @@ cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* im
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* img0, const uint8_t* mask0,
+                               int32_t* S0, float* inv0, const uint8_t* img1, const uint8_t* mask1, int32_t* S1,
+                               float* inv1, cudaStream_t st) {
+  return block_stats_t<uint8_t>(B, H, W, rho_b, img0, mask0, S0, inv0, img1, mask1, S1, inv1, st);
+}
+
+cudaError_t launch_block_stats16(int B, int H, int W, int rho_b, const uint8_t* img0, int32_t* S0, float* inv0,
+                                 const uint16_t* img1, const uint8_t* mask1, int32_t* S1, float* inv1,
+                                 cudaStream_t st) {
+  return block_stats_t<uint16_t>(B, H, W, rho_b, img0, nullptr, S0, inv0, img1, mask1, S1, inv1, st);
 }
 
 // ---------------------------------------------------------------------------

@@ -262,3 +262,111 @@ def rsr_search_range(disparity, shift, delta, d_lo_limit, d_hi_limit, out=None):
     check("rsr_search_range", lib().rsr_search_range(RsrShape(B, H, W), _ptr(disparity), _ptr(shift), int(delta),
                                                      int(d_lo_limit), int(d_hi_limit), _ptr(out), _stream()))
     return out
+
+
+# --------------------------------------------------------------------------- #
+# Interpolating-warp variant (NEXT row f2; include/rsr.h, reading 21)
+# --------------------------------------------------------------------------- #
+def rsr_warp_linear(target, alpha_beta, warped=None, valid=None, shift=None):
+    """Step 1' (linear interpolation at 1/256-px positions): returns (warped uint16
+    [B,H,W] in 8.8 fixed point, valid uint8 [B,H,W], shift float64 [B,H] = t_q(v))."""
+    target, s = _bhw(target)
+    B, H, W = target.shape
+    _expect(target, torch.uint8, (B, H, W), "target")
+    alpha_beta = alpha_beta.reshape(B, 2)
+    _expect(alpha_beta, torch.float64, (B, 2), "alpha_beta")
+    dev = target.device
+    warped = torch.empty((B, H, W), dtype=torch.uint16, device=dev) if warped is None else warped
+    valid = torch.empty_like(target) if valid is None else valid
+    shift = torch.empty((B, H), dtype=torch.float64, device=dev) if shift is None else shift
+    _expect(warped, torch.uint16, (B, H, W), "warped")
+    _expect(valid, torch.uint8, (B, H, W), "valid")
+    _expect(shift, torch.float64, (B, H), "shift")
+    check("rsr_warp_linear", lib().rsr_warp_linear(s, _ptr(alpha_beta), _ptr(target), _ptr(warped), _ptr(valid),
+                                                   _ptr(shift), _stream()))
+    return warped, valid, shift
+
+
+def rsr_cost_volume_linear(ref, warped, valid, rho_block, d_lo, d_hi, *, with_tar=True, with_nan_maps=True,
+                           vol_ref=None, vol_tar=None, nan_ref=None, nan_tar=None, workspace=None):
+    """Step 2 on (uint8 ref, uint16 8.8 warped): (vol_ref, vol_tar|None, nan_ref|None, nan_tar|None)."""
+    ref, s = _bhw(ref)
+    B, H, W = ref.shape
+    warped, _ = _bhw(warped)
+    valid, _ = _bhw(valid)
+    D = d_hi - d_lo + 1
+    if D < 1:
+        raise ValueError(f"rsr: empty search range [{d_lo}, {d_hi}]")
+    _expect(ref, torch.uint8, (B, H, W), "ref")
+    _expect(warped, torch.uint16, (B, H, W), "warped")
+    _expect(valid, torch.uint8, (B, H, W), "valid")
+    dev = ref.device
+    if vol_ref is None:
+        vol_ref = torch.empty((B, H, W, D), dtype=torch.float32, device=dev)
+    if with_tar and vol_tar is None:
+        vol_tar = torch.empty((B, H, W, D), dtype=torch.float32, device=dev)
+    if with_nan_maps:
+        nan_ref = torch.empty((B, H, W), dtype=torch.uint8, device=dev) if nan_ref is None else nan_ref
+        if with_tar and nan_tar is None:
+            nan_tar = torch.empty((B, H, W), dtype=torch.uint8, device=dev)
+    nbytes = cost_workspace_bytes(B, H, W)
+    if workspace is None:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    for t, name in ((vol_ref, "vol_ref"), (vol_tar, "vol_tar")):
+        _expect(t, torch.float32, (B, H, W, D), name)
+    for t, name in ((nan_ref, "nan_ref"), (nan_tar, "nan_tar")):
+        _expect(t, torch.uint8, (B, H, W), name)
+    if workspace.dtype != torch.uint8 or workspace.dim() != 1 or workspace.numel() < nbytes:
+        raise ValueError(f"rsr: workspace must be a uint8 vector of >= {nbytes} bytes")
+    check("rsr_cost_volume_linear", lib().rsr_cost_volume_linear(
+        s, RsrCostParams(rho_block, d_lo, d_hi), _ptr(ref), _ptr(warped), _ptr(valid), _ptr(vol_ref),
+        _ptr(vol_tar), _ptr(nan_ref), _ptr(nan_tar), _ptr(workspace), workspace.numel(), _stream()))
+    return vol_ref, vol_tar, nan_ref, nan_tar
+
+
+def rsr_aggregate_linear(vol, guide, rho, gamma_d, gamma_r, nan_map=None, out=None, concurrency=1):
+    """Step 3 with a uint16 8.8 fixed-point guide (the target volume of the interpolating warp)."""
+    guide, s = _bhw(guide)
+    B, H, W = guide.shape
+    if vol.dim() == 3:
+        vol = vol.unsqueeze(0)
+    D = vol.shape[-1]
+    _expect(guide, torch.uint16, (B, H, W), "guide")
+    _expect(vol, torch.float32, (B, H, W, D), "vol")
+    out = torch.empty_like(vol) if out is None else out
+    _expect(out, torch.float32, (B, H, W, D), "out")
+    if out.data_ptr() == vol.data_ptr():
+        raise ValueError("rsr: out must not alias vol")
+    if nan_map is not None:
+        nan_map, _ = _bhw(nan_map)
+        _expect(nan_map, torch.uint8, (B, H, W), "nan_map")
+    check("rsr_aggregate_linear", lib().rsr_aggregate_linear(
+        s, D, RsrAggParams(rho, float(gamma_d), float(gamma_r), int(concurrency)), _ptr(vol), _ptr(guide),
+        _ptr(nan_map), _ptr(out), _stream()))
+    return out
+
+
+def rsr_disparity_linear(agg_ref, agg_tar, shift, d_lo, d_hi, lrc_tol, subpixel=True, disparity=None,
+                         wta_ref=None, wta_tar=None, with_wta=False):
+    """Steps 4-5 with the fp64 applied shift t_q(v) (float64 [B,H]) of rsr_warp_linear."""
+    if agg_ref.dim() == 3:
+        agg_ref, agg_tar = agg_ref.unsqueeze(0), agg_tar.unsqueeze(0)
+    B, H, W, D = agg_ref.shape
+    if D != d_hi - d_lo + 1:
+        raise ValueError(f"rsr: volumes hold D = {D} disparities, range [{d_lo}, {d_hi}] needs {d_hi - d_lo + 1}")
+    _expect(agg_ref, torch.float32, (B, H, W, D), "agg_ref")
+    _expect(agg_tar, torch.float32, (B, H, W, D), "agg_tar")
+    shift = shift.reshape(B, H)
+    _expect(shift, torch.float64, (B, H), "shift")
+    dev = agg_ref.device
+    disparity = torch.empty((B, H, W), dtype=torch.float32, device=dev) if disparity is None else disparity
+    if with_wta:
+        wta_ref = torch.empty((B, H, W), dtype=torch.int16, device=dev) if wta_ref is None else wta_ref
+        wta_tar = torch.empty((B, H, W), dtype=torch.int16, device=dev) if wta_tar is None else wta_tar
+    _expect(disparity, torch.float32, (B, H, W), "disparity")
+    _expect(wta_ref, torch.int16, (B, H, W), "wta_ref")
+    _expect(wta_tar, torch.int16, (B, H, W), "wta_tar")
+    check("rsr_disparity_linear", lib().rsr_disparity_linear(
+        RsrShape(B, H, W), RsrDispParams(d_lo, d_hi, lrc_tol, 1 if subpixel else 0), _ptr(agg_ref),
+        _ptr(agg_tar), _ptr(shift), _ptr(disparity), _ptr(wta_ref), _ptr(wta_tar), _stream()))
+    return disparity, wta_ref, wta_tar

@@ -23,15 +23,16 @@ class StereoParams:
     focal: float = 700.0
     baseline: float = 0.12
     d_min: float = 1.0
+    warp: str = "integer"    # "integer" (reading 1, rsr_warp) or "linear" (NEXT f2, rsr_warp_linear)
 
     @property
     def D(self):
         return self.d_hi - self.d_lo + 1
 
     @staticmethod
-    def from_config(cfg):
+    def from_config(cfg, warp="integer"):
         return StereoParams(cfg.d_lo, cfg.d_hi, cfg.rho_block, cfg.rho_agg, cfg.gamma_d, cfg.gamma_r,
-                            cfg.lrc_tol, True, cfg.focal, cfg.baseline)
+                            cfg.lrc_tol, True, cfg.focal, cfg.baseline, warp=warp)
 
 
 class StereoPipeline:
@@ -51,9 +52,12 @@ class StereoPipeline:
         D = params.D
         dev = torch.device(device)
         e = lambda shape, dt: torch.empty(shape, dtype=dt, device=dev)  # noqa: E731
-        self.warped = e((B, H, W), torch.uint8)
+        if params.warp not in ("integer", "linear"):
+            raise ValueError(f"unknown warp {params.warp!r}")
+        self.linear = params.warp == "linear"
+        self.warped = e((B, H, W), torch.uint16 if self.linear else torch.uint8)
         self.valid = e((B, H, W), torch.uint8)
-        self.shift = e((B, H), torch.int32)
+        self.shift = e((B, H), torch.float64 if self.linear else torch.int32)
         self.vol_ref = e((B, H, W, D), torch.float32)
         self.vol_tar = e((B, H, W, D), torch.float32)
         self.nan_ref = e((B, H, W), torch.uint8)
@@ -69,10 +73,11 @@ class StereoPipeline:
 
     def run(self, left, right, alpha_beta, with_wta=True):
         p = self.p
-        ops.rsr_warp(right, alpha_beta, self.warped, self.valid, self.shift)
-        ops.rsr_cost_volume(left, self.warped, self.valid, p.rho_block, p.d_lo, p.d_hi,
-                            vol_ref=self.vol_ref, vol_tar=self.vol_tar, nan_ref=self.nan_ref,
-                            nan_tar=self.nan_tar, workspace=self.workspace)
+        lin = self.linear
+        (ops.rsr_warp_linear if lin else ops.rsr_warp)(right, alpha_beta, self.warped, self.valid, self.shift)
+        (ops.rsr_cost_volume_linear if lin else ops.rsr_cost_volume)(
+            left, self.warped, self.valid, p.rho_block, p.d_lo, p.d_hi, vol_ref=self.vol_ref,
+            vol_tar=self.vol_tar, nan_ref=self.nan_ref, nan_tar=self.nan_tar, workspace=self.workspace)
         # the two aggregations are independent: the target volume's on a side stream, so
         # each launch back-fills the other's last wave
         main = torch.cuda.current_stream()
@@ -81,16 +86,17 @@ class StereoPipeline:
         fork = torch.cuda.Event()
         fork.record(main)
         self._side.wait_event(fork)
+        aggregate_tar = ops.rsr_aggregate_linear if lin else ops.rsr_aggregate
         with torch.cuda.stream(self._side):
-            ops.rsr_aggregate(self.vol_tar, self.warped, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_tar,
-                              self.agg_tar, concurrency=2)
+            aggregate_tar(self.vol_tar, self.warped, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_tar,
+                          self.agg_tar, concurrency=2)
         ops.rsr_aggregate(self.vol_ref, left, p.rho_agg, p.gamma_d, p.gamma_r, self.nan_ref, self.agg_ref,
                           concurrency=2)
         join = torch.cuda.Event()
         join.record(self._side)
         main.wait_event(join)
-        ops.rsr_disparity(self.agg_ref, self.agg_tar, self.shift, p.d_lo, p.d_hi, p.lrc_tol, p.subpixel,
-                          self.disparity, self.wta_ref if with_wta else None,
-                          self.wta_tar if with_wta else None)
+        disparity = ops.rsr_disparity_linear if lin else ops.rsr_disparity
+        disparity(self.agg_ref, self.agg_tar, self.shift, p.d_lo, p.d_hi, p.lrc_tol, p.subpixel,
+                  self.disparity, self.wta_ref if with_wta else None, self.wta_tar if with_wta else None)
         ops.rsr_reconstruct(self.disparity, p.focal, p.baseline, d_min=p.d_min, xyz=self.xyz)
         return self.disparity
