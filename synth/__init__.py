@@ -27,7 +27,8 @@ import math
 
 import numpy as np
 
-__all__ = ["StereoConfig", "Frame", "CONFIGS", "get_config", "make_frame", "make_batch"]
+__all__ = ["StereoConfig", "Frame", "CONFIGS", "get_config", "make_frame", "make_batch", "make_sequence",
+           "box_disparity_gain"]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -58,6 +59,9 @@ class StereoConfig:
     seed: int = 1
     batch: int = 1
     random_plane: bool = False  # config 5: alpha~U[0.08,0.12], beta~U[25,35] per frame
+    # accuracy scene (NEXT f4): a box ("sample model") of known height standing
+    # on the road, (u0, v0, u1, v1, height_m) in reference-image pixels / metres
+    box: tuple | None = None
 
     @property
     def D(self) -> int:
@@ -119,12 +123,30 @@ def _value_noise(rng: np.random.Generator, h: int, w: int) -> np.ndarray:
     return 40.0 + (tex - lo) * (180.0 / (hi - lo))
 
 
+def box_disparity_gain(cfg: StereoConfig, alpha: float, beta: float, height_m: float) -> float:
+    """Disparity gain kappa of the top face of a box of height h on the road plane.
+
+    Scene geometry, not the method: with the rectified pinhole of reading 15
+    (u0 = (W-1)/2, v0 = (H-1)/2), the road d = alpha v + beta is the 3-D plane
+    alpha f Y + (alpha v0 + beta) Z = f b (normal norm |n|); the parallel plane
+    at height h towards the camera projects to d' = kappa (alpha v + beta),
+    kappa = f b / (f b - h |n|)."""
+    v0 = (cfg.height - 1) / 2.0
+    nrm = math.hypot(alpha * cfg.focal, alpha * v0 + beta)
+    fb = cfg.focal * cfg.baseline
+    return fb / (fb - height_m * nrm)
+
+
 class _Scene:
     """Analytic ground-truth disparity d(x, v) over the reference view."""
 
     def __init__(self, cfg: StereoConfig, rng: np.random.Generator, alpha: float, beta: float):
         h, w = cfg.height, cfg.width
         self.alpha, self.beta = alpha, beta
+        self.box = None
+        if cfg.box is not None:
+            u0, v0, u1, v1, hb = cfg.box
+            self.box = (u0, v0, u1, v1, box_disparity_gain(cfg, alpha, beta, hb))
         s = cfg.pothole_sigma
         m = 3.0 * s
         self.pots = []
@@ -150,6 +172,10 @@ class _Scene:
 
     def disparity(self, x: np.ndarray, y: np.ndarray) -> np.ndarray:
         d = self.alpha * y + self.beta
+        if self.box is not None:
+            u0, v0, u1, v1, kappa = self.box
+            inside = (x >= u0) & (x < u1) & (y >= v0) & (y < v1)
+            d = np.where(inside, kappa * d, d)
         for cx, cy in self.pots:
             d = d + self.amp * np.exp(-((x - cx) ** 2 + (y - cy) ** 2) / (2.0 * self.sig ** 2))
         if self.crack is not None:
@@ -171,10 +197,22 @@ def make_frame(cfg: StereoConfig, index: int = 0) -> Frame:
         beta = float(rng.uniform(25.0, 35.0))
     h, w = cfg.height, cfg.width
     # texture wide enough for x_l = x + d up to the largest disparity
-    d_max_est = abs(alpha) * h + abs(beta) + 4.0
-    wt = w + int(math.ceil(d_max_est)) + 4
+    wt = _texture_width(cfg, alpha, beta)
     tex = _value_noise(rng, h, wt)
     scene = _Scene(cfg, rng, alpha, beta)
+    return _render(cfg, rng, tex, scene, alpha, beta)
+
+
+def _texture_width(cfg, alpha, beta):
+    d_max_est = abs(alpha) * cfg.height + abs(beta) + 4.0
+    if cfg.box is not None:
+        d_max_est *= 1.2
+    return cfg.width + int(math.ceil(d_max_est)) + 4
+
+
+def _render(cfg, rng, tex, scene, alpha, beta) -> Frame:
+    h, w = cfg.height, cfg.width
+    wt = tex.shape[1]
     ys = np.arange(h, dtype=np.float64)[:, None]
     xs = np.arange(w, dtype=np.float64)[None, :]
     d_gt = scene.disparity(np.broadcast_to(xs, (h, w)), np.broadcast_to(ys, (h, w)))
@@ -194,6 +232,34 @@ def make_frame(cfg: StereoConfig, index: int = 0) -> Frame:
     right = np.clip(np.rint(right_f), 0, 255).astype(np.uint8)
     excl = scene.exclude(np.broadcast_to(xs, (h, w)), np.broadcast_to(ys, (h, w)))
     return Frame(left, right, alpha, beta, d_gt, excl)
+
+
+def make_sequence(cfg: StereoConfig, n: int, scroll: int = 3, dalpha: float = 1e-4, dbeta: float = 0.05):
+    """A video-like sequence of n frames (restricted-search-range evaluation):
+    the vehicle moves forward, so the road texture (and its potholes / crack)
+    scrolls down by ``scroll`` rows per frame, and the road plane drifts slowly
+    (alpha_t = alpha + t dalpha, beta_t = beta + t dbeta).  Fresh sensor noise per
+    frame.  Deterministic in cfg.seed."""
+    rng = np.random.Generator(np.random.PCG64(cfg.seed + 7_000_000))
+    h, w = cfg.height, cfg.width
+    a_max, b_max = cfg.alpha + n * abs(dalpha), cfg.beta + n * abs(dbeta)
+    wt = _texture_width(cfg, a_max, b_max)
+    tall = _value_noise(rng, h + n * scroll, wt)
+    base = _Scene(cfg, rng, cfg.alpha, cfg.beta)
+    frames = []
+    for t in range(n):
+        alpha, beta = cfg.alpha + t * dalpha, cfg.beta + t * dbeta
+        off = (n - 1 - t) * scroll               # texture window moves up: content moves down
+        tex = tall[off:off + h]
+        scene = _Scene.__new__(_Scene)
+        scene.__dict__.update(base.__dict__)
+        scene.alpha, scene.beta = alpha, beta
+        scene.pots = [(cx, cy + t * scroll) for cx, cy in base.pots]
+        if base.crack is not None:
+            p, q = base.crack
+            scene.crack = (p + np.array([0.0, t * scroll]), q + np.array([0.0, t * scroll]))
+        frames.append(_render(cfg, rng, tex, scene, alpha, beta))
+    return frames
 
 
 def make_batch(cfg: StereoConfig, indices) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
