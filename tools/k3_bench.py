@@ -52,5 +52,6 @@ if __name__ == "__main__":
     if len(sys.argv) > 1:   # one case: B H W D rho nan_band [reps]
         a = sys.argv[1:]
         cases = [(int(a[0]), int(a[1]), int(a[2]), int(a[3]), int(a[4]), float(a[5]))]
-    for c in cases:
-        print(json.dumps(bench(*c, reps=int(os.environ.get("REPS", "5")))), flush=True)
+    from _clocks import run_with_clocks
+    run_with_clocks(lambda: [print(json.dumps(bench(*c, reps=int(os.environ.get("REPS", "5")))), flush=True)
+                             for c in cases], "k3_bench")

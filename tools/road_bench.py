@@ -53,4 +53,5 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    from _clocks import run_with_clocks
+    run_with_clocks(main, "road_bench")
