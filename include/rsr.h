@@ -223,6 +223,27 @@ int rsr_disparity_linear(rsr_shape s, rsr_disp_params p, const float* agg_ref,
                          int16_t* wta_ref, int16_t* wta_tar, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Fused, volume-free matching (NEXT row f1; P:106 shear identity, P:251     */
+/* "performing the bilateral filtering on the whole cost volume is a very   */
+/* time-consuming process").  Steps 2-5a in one kernel over row strips: the  */
+/* NCC costs of Eqs. (3)-(5), the target volume by the shear                 */
+/* C_R(x', k) = C_L(x' + d_lo + k, k), the bilateral aggregation of both     */
+/* (Eqs. 8-10), WTA, the check of Eq. (11), Eq. (12) and the shift s(v) --   */
+/* no cost or aggregated volume is written.  Every value follows the         */
+/* operations of rsr_cost_volume / rsr_aggregate / rsr_disparity in the same */
+/* order, so disparity, wta_ref and wta_tar equal theirs bit for bit.        */
+/*   ref, warped, valid, shift : as produced for / by rsr_warp               */
+/*   disparity : float [B][H][W] out; wta_ref / wta_tar optional int16 out   */
+/*   workspace : rsr_cost_workspace_size(s) bytes (block statistics)         */
+/* Errors: as rsr_cost_volume / rsr_aggregate / rsr_disparity, plus          */
+/* RSR_E_ARG unless D = d_hi - d_lo + 1 <= 8 (the small search ranges of the */
+/* restricted band), rho <= 7, dp's range equal to cp's and 2B <= 65535.     */
+int rsr_match(rsr_shape s, rsr_cost_params cp, rsr_agg_params ap, rsr_disp_params dp,
+              const uint8_t* ref, const uint8_t* warped, const uint8_t* valid,
+              const int32_t* shift, float* disparity, int16_t* wta_ref,
+              int16_t* wta_tar, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Road model (before the path: Eq. (2)).  Robust least-squares fit */
 /* of the road's v-disparity line d = alpha * v + beta ("estimated by solving */
 /* a least squares problem with a collection of reliable correspondence      */

@@ -10,5 +10,6 @@ from .ops import (rsr_aggregate, rsr_cost_volume, rsr_disparity, rsr_reconstruct
                   rsr_warp, rsr_road_model, rsr_road_roll, rsr_plane_fit, rsr_plane_distance,
                   rsr_search_range, rsr_aggregate_rows,
                   rsr_warp_linear, rsr_cost_volume_linear, rsr_aggregate_linear, rsr_disparity_linear,
+                  rsr_match,
                   cost_workspace_bytes)
 from .pipeline import StereoParams, StereoPipeline  # noqa: F401

@@ -74,6 +74,9 @@ def lib() -> ctypes.CDLL:
         L.rsr_disparity_linear.argtypes = [RsrShape, RsrDispParams, P, P, P, P, P, P, P]
         for f in ("rsr_warp_linear", "rsr_cost_volume_linear", "rsr_aggregate_linear", "rsr_disparity_linear"):
             getattr(L, f).restype = ctypes.c_int
+        L.rsr_match.argtypes = [RsrShape, RsrCostParams, RsrAggParams, RsrDispParams, P, P, P, P, P, P, P, P,
+                                ctypes.c_size_t, P]
+        L.rsr_match.restype = ctypes.c_int
         L.rsr_road_workspace_size.argtypes = [RsrShape, RsrRoadParams]
         L.rsr_road_workspace_size.restype = ctypes.c_size_t
         L.rsr_road_model.argtypes = [RsrShape, RsrRoadParams, P, P, P, ctypes.c_size_t, P]

@@ -311,6 +311,8 @@ size_t aggregate_tiled_smem(int D, int rho) { return agg_geom(D, rho).bytes; }
 cudaError_t launch_aggregate(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r, int conc,
                              const float* vol, const uint8_t* guide, const uint8_t* nan_map,
                              float* out, cudaStream_t st) {
+  if (aggregate_small_applies(D, rho))
+    return launch_aggregate_small(B, H, W, D, rho, gamma_d, gamma_r, conc, vol, guide, nan_map, out, st);
   if (rho <= 7)
     return launch_aggregate_slide(B, H, W, D, rho, gamma_d, gamma_r, conc, vol, guide, nan_map, out, st);
 #define RSR_A(R) \

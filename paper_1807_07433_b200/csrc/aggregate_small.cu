@@ -1,0 +1,377 @@
+// K3s — bilateral cost aggregation (Eq. (8) with Eqs. (9)-(10))
+// for SMALL disparity slabs (D <= 16, run as slabs of 8): the restricted search
+// range of P:251 ("reduce the search range and only perform the bilateral
+// filtering on the space around the calculated disparities") and tiny ranges.
+//
+// At D = 8 a bilateral weight w(p, q) feeds only 8 FMAs, so the producer/consumer
+// kernel (aggregate_slide.cu: 4 weight-producer warps, 1 consumer warp, weights
+// handed over through shared memory) is bound by weight production and runs one
+// FFMA2 warp per CTA (measured 15 % of FP32 at D = 8).  Here every thread owns one
+// output column x and all 8 disparities of the slab and computes its own weights:
+//   w(a, j) = S(a, j) * R(g(x + j - rho, y_in) - g(x, y_a))
+// with the spatial factors S in a broadcast shared table and the range factor R
+// in a shared table replicated per lane (lut[idx][lane]: every warp-wide lookup is
+// one conflict-free wavefront).  The strip slides down one input row at a time;
+// a thread keeps the 2 rho + 1 output rows ("ages") whose windows contain the
+// input row (13 x 4 packed pairs at rho = 6), so each staged cost feeds 2 rho + 1
+// FFMA2s, exactly as in aggregate_slide.cu.
+//
+// Arithmetic is that of aggregate_slide.cu operation for operation: the same
+// factors (ex2 of the same arguments), w = S * R, numerators fma(w, c, acc) and
+// denominators (the running sum of w, clean segments; fma(w, validity, acc),
+// general segments) in (input row, tap) order, and the same epilogues
+// (num * rcp(den)).  Results are therefore bitwise identical to that kernel's,
+// whichever segment / path a pixel falls in (tests/test_gpu_parity.py).
+#include <cmath>
+#include <cstdlib>
+#include <type_traits>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rsr {
+
+constexpr int SM_TX = 128;            // output columns per CTA (one per thread)
+constexpr int SM_KD = 8;              // disparities per slab
+constexpr int SM_LUT = 512;           // range table entries per lane: dg + 255 in [0, 510], 511 = 0
+constexpr int SM_SKIPQ = 4096;        // guide code of a skipped tap pixel (clamps to the zero entry)
+constexpr int SM_SKIPP = -4096;       // guide code of a skipped centre pixel
+
+struct SmallArgs {
+  int B, H, W, D, R, nslab;
+  float kd, kr;
+  const float* vol;
+  const uint8_t* guide;
+  const uint8_t* nan_map;
+  float* out;
+};
+
+template <int RHO>
+struct SmallGeom {
+  static constexpr int NT = 2 * RHO + 1;
+  static constexpr int CX = SM_TX + 2 * RHO;       // staged columns per input row
+  static constexpr int STW = NT <= 16 ? 16 : 32;   // spatial table row stride
+  // shared memory (bytes): lut | S | 2 cost rows [CX][8] | 2 guide rows [CX] (int)
+  static constexpr size_t off_lut = 0;
+  static constexpr size_t off_s = off_lut + sizeof(float) * SM_LUT * 32;
+  static constexpr size_t off_cost = off_s + sizeof(float) * NT * STW;
+  static constexpr size_t off_guide = off_cost + sizeof(float) * 2 * CX * SM_KD;
+  static constexpr size_t bytes = off_guide + sizeof(int) * 2 * CX;
+};
+
+template <int RHO>
+__global__ void __launch_bounds__(SM_TX, 2) k_aggregate_small(const SmallArgs A) {
+  using G = SmallGeom<RHO>;
+  constexpr int NT = G::NT, CX = G::CX;
+  extern __shared__ __align__(16) unsigned char sm_smem[];
+  float* lut = reinterpret_cast<float*>(sm_smem + G::off_lut);
+  float* S = reinterpret_cast<float*>(sm_smem + G::off_s);
+  float* cost = reinterpret_cast<float*>(sm_smem + G::off_cost);
+  int* grow = reinterpret_cast<int*>(sm_smem + G::off_guide);
+  const int tid = threadIdx.x, lane = tid & 31;
+
+  // ---- segment: 128 columns x R rows of frame b, disparity slab ----
+  const int nstrip = (A.W + SM_TX - 1) / SM_TX;
+  const int nchunk = (A.H + A.R - 1) / A.R;
+  int blk = blockIdx.x;
+  const int strip = blk % nstrip;
+  blk /= nstrip;
+  const int chunk = blk % nchunk;
+  blk /= nchunk;
+  const int slab = blk % A.nslab, b = blk / A.nslab;
+  const int x0 = strip * SM_TX, ya = chunk * A.R, yb = min(A.H, ya + A.R);
+  const int k0 = slab * SM_KD, ks_eff = min(SM_KD, A.D - k0);
+  const size_t pix0 = (size_t)b * A.H * A.W;
+  const int x = x0 + tid;
+
+  // ---- tables: range factor exp2(kr dg^2) per lane, spatial factor exp2(kd (dx^2 + dy^2)) ----
+  for (int e = tid; e < SM_LUT * 32; e += SM_TX) {
+    const int dg = e / 32 - 255;
+    lut[e] = (dg <= 255) ? ex2_ftz((float)(dg * dg) * A.kr) : 0.f;
+  }
+  // S[j][a]: tap j (dx = j - RHO), age a = output row y_in - RHO + a (dy = RHO - a);
+  // ages contiguous so four of them are one broadcast LDS.128
+  for (int e = tid; e < NT * G::STW; e += SM_TX) {
+    const int j = e / G::STW, a = e % G::STW;
+    S[e] = a < NT ? ex2_ftz((float)((j - RHO) * (j - RHO) + (RHO - a) * (RHO - a)) * A.kd) : 0.f;
+  }
+
+  // ---- classify: a partially-NaN pixel anywhere in the footprint -> general path ----
+  int partial = A.nan_map == nullptr ? 1 : 0;
+  if (!partial) {
+    const int fw = CX, fh = (yb - ya) + 2 * RHO;
+    for (int e = tid; e < fw * fh; e += SM_TX) {
+      const int yy = ya - RHO + e / fw, xx = x0 - RHO + e % fw;
+      if (yy >= 0 && yy < A.H && xx >= 0 && xx < A.W && (A.nan_map[pix0 + (size_t)yy * A.W + xx] & 3) == 3)
+        partial = 1;
+    }
+  }
+  const bool clean = !__syncthreads_or(partial);
+
+  // pixel class from nan_map: skipped (outside the image or all k NaN) or not
+  auto skipped = [&](int yy, int xx) {
+    if (yy < 0 || yy >= A.H || xx < 0 || xx >= A.W) return true;
+    return A.nan_map != nullptr && (A.nan_map[pix0 + (size_t)yy * A.W + xx] & 3) == 1;
+  };
+  auto guide_code = [&](int yy, int xx, bool centre) {
+    if (skipped(yy, xx)) return centre ? SM_SKIPP : SM_SKIPQ;
+    return (int)A.guide[pix0 + (size_t)yy * A.W + xx];
+  };
+
+  const int NR = (yb - ya) + 2 * RHO;   // input rows ya - RHO .. yb + RHO - 1
+  // the row loop, specialised on the path (clean / general) so each instantiation
+  // holds only its own registers
+  auto run = [&](auto clean_tag) {
+    constexpr bool CLEAN = decltype(clean_tag)::value;
+  const int npass = CLEAN ? 1 : 2;
+  for (int pass = 0; pass < npass; pass++) {
+    // staged values per column: clean: costs k0..k0+7 (NaN-free: skipped pixels and
+    // k >= D give 0); general pass h: (C0, V) pairs of k0 + 4h .. k0 + 4h + 3
+    auto fetch_row = [&](int i, float (&v)[2][SM_KD], int (&gv)[2]) {
+      const int yy = ya - RHO + i;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int c = tid + h * SM_TX;
+        gv[h] = 0;
+#pragma unroll
+        for (int q = 0; q < SM_KD; q++) v[h][q] = 0.f;
+        if (c >= CX) continue;
+        const int xx = x0 - RHO + c;
+        gv[h] = guide_code(yy, xx, false);
+        if (gv[h] == SM_SKIPQ) continue;       // weight 0; cost (0) or pair (0, 0)
+        const float* src = A.vol + (pix0 + (size_t)yy * A.W + xx) * A.D + k0;
+        if (CLEAN && ks_eff == SM_KD && (A.D & 3) == 0) {
+          const float4 t0 = __ldg(reinterpret_cast<const float4*>(src));
+          const float4 t1 = __ldg(reinterpret_cast<const float4*>(src + 4));
+          v[h][0] = t0.x; v[h][1] = t0.y; v[h][2] = t0.z; v[h][3] = t0.w;
+          v[h][4] = t1.x; v[h][5] = t1.y; v[h][6] = t1.z; v[h][7] = t1.w;
+        } else if (CLEAN) {
+#pragma unroll
+          for (int q = 0; q < SM_KD; q++) v[h][q] = q < ks_eff ? __ldg(src + q) : 0.f;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const int k = 4 * pass + q;
+            const float cv = k < ks_eff ? __ldg(src + k) : qnan();
+            const bool ok = !(cv != cv);
+            v[h][2 * q] = ok ? cv : 0.f;
+            v[h][2 * q + 1] = ok ? 1.f : 0.f;
+          }
+        }
+      }
+    };
+    auto commit_row = [&](int i, const float (&v)[2][SM_KD], const int (&gv)[2]) {
+      const int st = i & 1;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int c = tid + h * SM_TX;
+        if (c >= CX) continue;
+        float4* d = reinterpret_cast<float4*>(cost + ((size_t)st * CX + c) * SM_KD);
+        d[0] = make_float4(v[h][0], v[h][1], v[h][2], v[h][3]);
+        d[1] = make_float4(v[h][4], v[h][5], v[h][6], v[h][7]);
+        grow[st * CX + c] = gv[h];
+      }
+    };
+
+    float2 acc[NT][4];
+    float den[NT];
+    int gp[NT];   // guide code of the output row of each age (its centre pixel)
+#pragma unroll
+    for (int a = 0; a < NT; a++) {
+#pragma unroll
+      for (int q = 0; q < 4; q++) acc[a][q] = make_float2(0.f, 0.f);
+      den[a] = 0.f;
+      gp[a] = guide_code(ya - 2 * RHO + a, x, true);   // age a at input row 0: output row ya - 2 rho + a
+    }
+    // clean rows of a whole 8-disparity slab (16-byte aligned): staged by cp.async straight
+    // into shared memory; other rows go through registers (fetch_row / commit_row)
+    const bool async_rows = CLEAN && ks_eff == SM_KD && (A.D & 3) == 0;
+    auto stage_async = [&](int i) {
+      const int yy = ya - RHO + i;
+      const int st = i & 1;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int c = tid + h * SM_TX;
+        if (c >= CX) continue;
+        const int xx = x0 - RHO + c;
+        const int gv = guide_code(yy, xx, false);
+        grow[st * CX + c] = gv;
+        float* d = cost + ((size_t)st * CX + c) * SM_KD;
+        if (gv == SM_SKIPQ) {
+          reinterpret_cast<float4*>(d)[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+          reinterpret_cast<float4*>(d)[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+          const float* src = A.vol + (pix0 + (size_t)yy * A.W + xx) * A.D + k0;
+          cp_async16(d, src);
+          cp_async16(d + 4, src + 4);
+        }
+      }
+      cp_async_commit();
+    };
+    float pv[2][SM_KD];
+    int pg[2];
+    if (async_rows) {
+      stage_async(0);
+      cp_async_wait_all();
+    } else {
+      fetch_row(0, pv, pg);
+      commit_row(0, pv, pg);
+    }
+    __syncthreads();
+    for (int i = 0; i < NR; i++) {
+      // the next row lands in the other stage (last read in iteration i - 1) during the math
+      if (i + 1 < NR) {
+        if (async_rows) stage_async(i + 1);
+        else fetch_row(i + 1, pv, pg);
+      }
+      const int st = i & 1;
+      const float* crow = cost + ((size_t)st * CX + tid) * SM_KD;
+      const int* gr = grow + st * CX + tid;
+      float2 fin[4];
+      float fden = 0.f;
+#pragma unroll
+      for (int j = 0; j < NT; j++) {
+        const float4 ca = *reinterpret_cast<const float4*>(crow + j * SM_KD);
+        const float4 cb = *reinterpret_cast<const float4*>(crow + j * SM_KD + 4);
+        const float2 cp[4] = {make_float2(ca.x, ca.y), make_float2(ca.z, ca.w), make_float2(cb.x, cb.y),
+                              make_float2(cb.z, cb.w)};
+        const int gq = gr[j];
+#pragma unroll
+        for (int a4 = 0; a4 < (NT + 3) / 4; a4++) {
+          const float4 s4 = *reinterpret_cast<const float4*>(S + j * G::STW + 4 * a4);   // broadcast
+          const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+          for (int t = 0; t < 4; t++) {
+            const int a = 4 * a4 + t;
+            if (a < NT) {
+              const int idx = min(gq - gp[a] + 255, SM_LUT - 1);
+              const float w = sv[t] * lut[idx * 32 + lane];
+              if (j < NT - 1) {
+                if (CLEAN) den[a] += w;
+#pragma unroll
+                for (int q = 0; q < 4; q++) acc[a][q] = f2fma(make_float2(w, w), cp[q], acc[a][q]);
+              } else if (a == 0) {
+                // last tap of the row: age 0 completes, every other age moves one slot down
+                if (CLEAN) fden = den[0] + w;
+#pragma unroll
+                for (int q = 0; q < 4; q++) fin[q] = f2fma(make_float2(w, w), cp[q], acc[0][q]);
+              } else {
+                if (CLEAN) den[a - 1] = den[a] + w;
+#pragma unroll
+                for (int q = 0; q < 4; q++) acc[a - 1][q] = f2fma(make_float2(w, w), cp[q], acc[a][q]);
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; q++) acc[NT - 1][q] = make_float2(0.f, 0.f);
+      den[NT - 1] = 0.f;
+      // the output row of age 0 completes at input row i
+      const int y = ya - 2 * RHO + i;
+      if (y >= ya && x < A.W) {
+        float* o = A.out + (pix0 + (size_t)y * A.W + x) * A.D + k0;
+        if (CLEAN) {
+          const float inv = __frcp_rn(fden);   // fden == 0 exactly for a skipped centre: NaN
+          const float r[8] = {fin[0].x * inv, fin[0].y * inv, fin[1].x * inv, fin[1].y * inv,
+                              fin[2].x * inv, fin[2].y * inv, fin[3].x * inv, fin[3].y * inv};
+          if (ks_eff == SM_KD && (A.D & 3) == 0) {
+            reinterpret_cast<float4*>(o)[0] = make_float4(r[0], r[1], r[2], r[3]);
+            reinterpret_cast<float4*>(o)[1] = make_float4(r[4], r[5], r[6], r[7]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < SM_KD; q++)
+              if (q < ks_eff) o[q] = r[q];
+          }
+        } else {
+          const float* cv = A.vol + (pix0 + (size_t)y * A.W + x) * A.D + k0;
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const int k = 4 * pass + q;
+            if (k < ks_eff) {
+              const float c = __ldg(cv + k);
+              o[k] = (c != c) ? qnan() : fin[q].x * __frcp_rn(fin[q].y);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int a = 0; a + 1 < NT; a++) gp[a] = gp[a + 1];
+      gp[NT - 1] = guide_code(ya - 2 * RHO + i + NT, x, true);
+      if (i + 1 < NR) {
+        if (async_rows) cp_async_wait_all();
+        else commit_row(i + 1, pv, pg);
+      }
+      __syncthreads();
+    }
+  }
+  };
+  if (clean) run(std::true_type());
+  else run(std::false_type());
+}
+
+static int small_sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+bool aggregate_small_applies(int D, int rho) {
+  if (D > 2 * SM_KD || rho > 7) return false;
+  const char* e = getenv("RSR_K3_SMALL");   // experiment hook (tools/, tests): 0 disables
+  return !(e && e[0] == '0');
+}
+
+template <int RHO>
+static cudaError_t small_launch_t(int B, int H, int W, int D, float gamma_d, float gamma_r, int conc,
+                                  const float* vol, const uint8_t* guide, const uint8_t* nan_map, float* out,
+                                  cudaStream_t st) {
+  using G = SmallGeom<RHO>;
+  SmallArgs A;
+  A.B = B; A.H = H; A.W = W; A.D = D;
+  A.nslab = (D + SM_KD - 1) / SM_KD;
+  const int nstrip = (W + SM_TX - 1) / SM_TX;
+  // rows per CTA: minimise waves x (R + 2 rho) with 2 CTAs per SM, counting the
+  // aggregations the caller keeps in flight together
+  const long long cols = (long long)nstrip * B * A.nslab * (conc > 1 ? conc : 1);
+  const long long slots = 2LL * small_sm_count();
+  int bestR = H;
+  double best = 1e300;
+  for (int n = 1; n <= H; n++) {
+    const int R = (H + n - 1) / n;
+    if (R < 16 && n > 1) break;
+    const long long ctas = cols * ((H + R - 1) / R);
+    const double c = (double)((ctas + slots - 1) / slots) * (R + 2 * RHO);
+    if (c < best * 0.999) { best = c; bestR = R; }
+  }
+  A.R = bestR;
+  const float log2e = 1.4426950408889634f;
+  A.kd = -log2e / (gamma_d * gamma_d);
+  A.kr = std::isinf(gamma_r) ? -1e-30f : -log2e / (gamma_r * gamma_r);
+  A.vol = vol; A.guide = guide; A.nan_map = nan_map; A.out = out;
+  const long long nblk = (long long)nstrip * ((H + bestR - 1) / bestR) * A.nslab * B;
+  if (nblk > 0x7fffffffLL) return cudaErrorInvalidValue;
+  cudaError_t e = smem_optin((const void*)k_aggregate_small<RHO>, G::bytes);
+  if (e != cudaSuccess) return e;
+  k_aggregate_small<RHO><<<(unsigned)nblk, SM_TX, G::bytes, st>>>(A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_aggregate_small(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r, int conc,
+                                   const float* vol, const uint8_t* guide, const uint8_t* nan_map, float* out,
+                                   cudaStream_t st) {
+#define RSR_SM(R) \
+  case R: return small_launch_t<R>(B, H, W, D, gamma_d, gamma_r, conc, vol, guide, nan_map, out, st);
+  switch (rho) {
+    RSR_SM(0) RSR_SM(1) RSR_SM(2) RSR_SM(3) RSR_SM(4) RSR_SM(5) RSR_SM(6) RSR_SM(7)
+    default:
+      return cudaErrorInvalidValue;
+  }
+#undef RSR_SM
+}
+
+}  // namespace rsr

@@ -187,6 +187,37 @@ int rsr_disparity_linear(rsr_shape s, rsr_disp_params p, const float* agg_ref, c
                                              wta_ref, wta_tar, as_stream(stream)));
 }
 
+// ---- fused, volume-free matching (NEXT row f1) ----
+int rsr_match(rsr_shape s, rsr_cost_params cp, rsr_agg_params ap, rsr_disp_params dp, const uint8_t* ref,
+              const uint8_t* warped, const uint8_t* valid, const int32_t* shift, float* disparity,
+              int16_t* wta_ref, int16_t* wta_tar, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!shape_ok(s) || !ref || !warped || !valid || !shift || !disparity || !workspace) return RSR_E_ARG;
+  if (cp.rho_block < 1 || cp.rho_block > 7 || cp.d_hi < cp.d_lo) return RSR_E_ARG;
+  if (dp.d_lo != cp.d_lo || dp.d_hi != cp.d_hi || dp.lrc_tol < 0) return RSR_E_ARG;
+  const long long D = (long long)cp.d_hi - cp.d_lo + 1;
+  if (D > 8) return RSR_E_ARG;
+  if (ap.rho < 0 || ap.rho > 7) return RSR_E_ARG;
+  if (!(ap.gamma_d > 0.f) || std::isinf(ap.gamma_d) || !(ap.gamma_r > 0.f)) return RSR_E_ARG;
+  if (workspace_bytes < rsr_cost_workspace_size(s)) return RSR_E_ARG;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return RSR_E_ARG;
+  if (s.height < 2 * cp.rho_block + 1 || s.width < 2 * cp.rho_block + 1) return RSR_E_DATA;
+  if ((size_t)(s.height + 15) / 16 > 65535 || 2LL * s.batch > 65535) return RSR_E_ARG;
+  const size_t chunk = align16(sizeof(int32_t) * npix(s));
+  char* ws = static_cast<char*>(workspace);
+  int32_t* SL = reinterpret_cast<int32_t*>(ws);
+  float* iL = reinterpret_cast<float*>(ws + chunk);
+  int32_t* SW = reinterpret_cast<int32_t*>(ws + 2 * chunk);
+  float* iW = reinterpret_cast<float*>(ws + 3 * chunk);
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = rsr::launch_block_stats(s.batch, s.height, s.width, cp.rho_block, ref, nullptr, SL, iL, warped,
+                                          valid, SW, iW, st);
+  if (e == cudaSuccess)
+    e = rsr::launch_match_fused(s.batch, s.height, s.width, cp.rho_block, cp.d_lo, (int)D, ap.rho, ap.gamma_d,
+                                ap.gamma_r, dp.lrc_tol, dp.subpixel != 0, ref, warped, shift, SL, iL, SW, iW,
+                                disparity, wta_ref, wta_tar, st);
+  return launched(e);
+}
+
 size_t rsr_road_workspace_size(rsr_shape s, rsr_road_params p) {
   if (!shape_ok(s) || p.step_u < 1 || p.step_v < 1 || p.n_hyp < 1) return 0;
   return rsr::road_workspace_size(s.batch, s.height, s.width, p.step_u, p.step_v, p.n_hyp);

@@ -94,6 +94,13 @@ RSR_DEVINL void cp_async8(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
 }
 
+// 16-byte asynchronous global -> shared copy (cp.async.cg, L2 only), group-tracked
+RSR_DEVINL void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+RSR_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+RSR_DEVINL void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // arrive on bar once every cp.async this thread issued so far has landed (counts as
 // one of the barrier's expected arrivals)
 RSR_DEVINL void cp_async_mbar_arrive_noinc(uint64_t* bar) {

@@ -148,28 +148,97 @@ __global__ void __launch_bounds__(256) k_disparity(int H, int W, int d_lo, int D
   }
 }
 
+// Small search ranges (D <= 16: the restricted band of P:251): one thread per pixel
+// scans its D costs (a pixel is 32-64 contiguous bytes; a warp's loads cover 32
+// consecutive pixels), instead of an 8-lane group of which only D/4 lanes would
+// load.  Same WTA rule (first index of the maximum over non-NaN entries), same
+// Eq. (11)-(12) arithmetic: results identical to k_disparity.
+RSR_DEVINL int pixel_argmax(const float* __restrict__ p, int D) {
+  float best = -INFINITY;
+  int kb = -1;
+  float v[16];
+#pragma unroll
+  for (int k = 0; k < 16; k++) v[k] = k < D ? __ldg(p + k) : qnan();
+#pragma unroll
+  for (int k = 0; k < 16; k++)
+    if (v[k] > best) { best = v[k]; kb = k; }   // NaN never compares greater
+  return kb;
+}
+
+template <typename ShiftT>
+__global__ void __launch_bounds__(256) k_disparity_small(int H, int W, int d_lo, int D, int tol, int subpix,
+                                                         const float* __restrict__ agg_ref,
+                                                         const float* __restrict__ agg_tar,
+                                                         const ShiftT* __restrict__ shift,
+                                                         float* __restrict__ disp,
+                                                         int16_t* __restrict__ wta_ref,
+                                                         int16_t* __restrict__ wta_tar) {
+  extern __shared__ int16_t krs_s[];  // [W]
+  const int v = blockIdx.x, b = blockIdx.y;
+  const size_t row = ((size_t)b * H + v) * W;
+  for (int u = threadIdx.x; u < W; u += blockDim.x) {
+    const int k = pixel_argmax(agg_tar + (row + u) * D, D);
+    krs_s[u] = (int16_t)k;
+    if (wta_tar) wta_tar[row + u] = (int16_t)k;
+  }
+  __syncthreads();
+  const ShiftT sv = shift[(size_t)b * H + v];
+  for (int u = threadIdx.x; u < W; u += blockDim.x) {
+    const float* p = agg_ref + (row + u) * D;
+    const int k = pixel_argmax(p, D);
+    if (wta_ref) wta_ref[row + u] = (int16_t)k;
+    float d = qnan();
+    if (k >= 0) {
+      const int up = u - (k + d_lo);
+      if (up >= 0 && up < W) {
+        const int kr = krs_s[up];
+        if (kr >= 0 && abs(k - kr) <= tol) {
+          float r = (float)(k + d_lo);
+          if (subpix && k >= 1 && k <= D - 2) {
+            const float a = p[k - 1], bb = p[k], c = p[k + 1];
+            const float den = 2.f * a + 2.f * c - 4.f * bb;
+            if (!(a != a) && !(c != c) && fabsf(den) > 1e-12f) r += __fdiv_rn(a - c, den);
+          }
+          d = sizeof(ShiftT) == 4 ? r + (float)sv : (float)((double)r + (double)sv);
+        }
+      }
+    }
+    disp[row + u] = d;
+  }
+}
+
+template <typename ShiftT>
+static cudaError_t disparity_launch_t(int B, int H, int W, int d_lo, int D, int tol, int subpix,
+                                      const float* agg_ref, const float* agg_tar, const ShiftT* shift,
+                                      float* disp, int16_t* wta_ref, int16_t* wta_tar, cudaStream_t st) {
+  const size_t smem = sizeof(int16_t) * (size_t)W;
+  dim3 grid(H, B);
+  if (D <= 16) {
+    const cudaError_t e = smem_optin((const void*)k_disparity_small<ShiftT>, smem);
+    if (e != cudaSuccess) return e;
+    k_disparity_small<ShiftT><<<grid, 256, smem, st>>>(H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, shift, disp,
+                                                       wta_ref, wta_tar);
+  } else {
+    const cudaError_t e = smem_optin((const void*)k_disparity<ShiftT>, smem);
+    if (e != cudaSuccess) return e;
+    k_disparity<ShiftT><<<grid, 256, smem, st>>>(H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, shift, disp,
+                                                 wta_ref, wta_tar);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_disparity(int B, int H, int W, int d_lo, int D, int tol, int subpix,
                              const float* agg_ref, const float* agg_tar, const int32_t* shift,
                              float* disp, int16_t* wta_ref, int16_t* wta_tar, cudaStream_t st) {
-  const size_t smem = sizeof(int16_t) * (size_t)W;
-  const cudaError_t e = smem_optin((const void*)k_disparity<int32_t>, smem);
-  if (e != cudaSuccess) return e;
-  dim3 grid(H, B);
-  k_disparity<int32_t><<<grid, 256, smem, st>>>(H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, shift, disp,
-                                                wta_ref, wta_tar);
-  return cudaGetLastError();
+  return disparity_launch_t<int32_t>(B, H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, shift, disp, wta_ref,
+                                     wta_tar, st);
 }
 
 cudaError_t launch_disparity_frac(int B, int H, int W, int d_lo, int D, int tol, int subpix,
                                   const float* agg_ref, const float* agg_tar, const double* shift,
                                   float* disp, int16_t* wta_ref, int16_t* wta_tar, cudaStream_t st) {
-  const size_t smem = sizeof(int16_t) * (size_t)W;
-  const cudaError_t e = smem_optin((const void*)k_disparity<double>, smem);
-  if (e != cudaSuccess) return e;
-  dim3 grid(H, B);
-  k_disparity<double><<<grid, 256, smem, st>>>(H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, shift, disp,
-                                               wta_ref, wta_tar);
-  return cudaGetLastError();
+  return disparity_launch_t<double>(B, H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, shift, disp, wta_ref,
+                                    wta_tar, st);
 }
 
 }  // namespace rsr

@@ -54,6 +54,12 @@ cudaError_t launch_aggregate_slide(int B, int H, int W, int D, int rho, float ga
                                    float gamma_r, int conc, const float* vol, const uint8_t* guide,
                                    const uint8_t* nan_map, float* out, cudaStream_t st);
 size_t aggregate_slide_smem(int D, int rho, int H);
+// small disparity slabs (D <= 16, rho <= 7): per-thread weights (aggregate_small.cu),
+// bitwise identical to the sliding kernel; RSR_K3_SMALL=0 disables (A/B, tests)
+bool aggregate_small_applies(int D, int rho);
+cudaError_t launch_aggregate_small(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r, int conc,
+                                   const float* vol, const uint8_t* guide, const uint8_t* nan_map, float* out,
+                                   cudaStream_t st);
 // the same with an 8.8 fixed-point (uint16) guide (interpolating warp, NEXT f2); rho <= 7
 cudaError_t launch_aggregate_slide16(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r, int conc,
                                      const float* vol, const uint16_t* guide, const uint8_t* nan_map,
@@ -69,6 +75,13 @@ cudaError_t launch_disparity(int B, int H, int W, int d_lo, int D, int tol, int 
 cudaError_t launch_disparity_frac(int B, int H, int W, int d_lo, int D, int tol, int subpix,
                                   const float* agg_ref, const float* agg_tar, const double* shift,
                                   float* disp, int16_t* wta_ref, int16_t* wta_tar, cudaStream_t st);
+
+// fused, volume-free matching for D <= 8 (NEXT f1, match_fused.cu): NCC -> both
+// aggregations -> WTA / LRC / subpixel / shift in one kernel, from the block statistics
+cudaError_t launch_match_fused(int B, int H, int W, int rho_b, int d_lo, int D, int rho, float gamma_d,
+                               float gamma_r, int lrc_tol, int subpix, const uint8_t* ref, const uint8_t* warped,
+                               const int32_t* shift, const int32_t* SL, const float* iL, const int32_t* SW,
+                               const float* iW, float* disp, int16_t* wta_ref, int16_t* wta_tar, cudaStream_t st);
 
 cudaError_t launch_reconstruct(int B, int H, int W, double f, double baseline, double u0,
                                double v0, double d_min, const float* disp, float* xyz,

@@ -165,7 +165,12 @@ cudaError_t launch_block_stats16(int B, int H, int W, int rho_b, const uint8_t* 
 // ---------------------------------------------------------------------------
 constexpr int ZX = 4;     // columns per thread
 constexpr int ZR = 8;     // disparities per thread (4 packed pairs)
-constexpr int ZTX = 64;   // columns per CTA (16 column groups)
+constexpr int ZTX = 64;   // columns per CTA (16 column groups) for D > 16
+// Small search ranges (D <= 16, e.g. the restricted band of P:251) use ZT = 256
+// columns per CTA so that the 128 threads stay busy (one disparity group of 8 per
+// column group of 4: 64 column groups x up to 2 disparity groups).
+constexpr int ZT_SMALL = 256;
+__host__ __device__ constexpr int zncc_cta_cols(int D) { return D <= 16 ? ZT_SMALL : ZTX; }
 constexpr int ZBY = 72;   // output rows per CTA (measured: 72 beats 48/60/80/90/96/144 at c5)
 
 // Shared-memory rows are stored "oriented": the G-side image row and G-side
@@ -178,7 +183,7 @@ struct ZnccGeom {
   int FC, GC, SGC, gpad, NRING, GROW, SROW2, RB, RS;
 };
 
-__host__ __device__ inline ZnccGeom zncc_geom(int p, int D) {
+__host__ __device__ inline ZnccGeom zncc_geom(int p, int D, int ZTX = rsr::ZTX) {
   ZnccGeom g;
   const int NJ = ZX + 2 * p;
   // image rows y-1 .. y+2p being read, plus the one committed for the next row into
@@ -196,14 +201,14 @@ __host__ __device__ inline ZnccGeom zncc_geom(int p, int D) {
   return g;
 }
 
-__host__ __device__ inline size_t zncc_smem(int p, int D) {
-  const ZnccGeom g = zncc_geom(p, D);
+__host__ __device__ inline size_t zncc_smem(int p, int D, int ZTX = rsr::ZTX) {
+  const ZnccGeom g = zncc_geom(p, D, ZTX);
   // ring: F rows, oriented G rows x2; statistics double buffer: sF, iF, sG x2, iG x2
   return sizeof(float) * ((size_t)g.NRING * (g.FC + 2 * g.GROW) + 2 * (2 * ZTX + 4 * (size_t)g.SROW2));
 }
 
 // One CTA of the volume kernel for frame b (the kernels below pick b and TAR).
-template <int P, bool TAR>
+template <int P, bool TAR, int ZTX = rsr::ZTX>
 __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, int Dst, int koff,
                                               const uint8_t* __restrict__ ref,
                                               const uint8_t* __restrict__ warped,
@@ -218,7 +223,7 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
   constexpr int NF4 = (NJ + 3) / 4, NG4 = (NGR + 3) / 4;
   constexpr int NSR = ZX + ZR;            // oriented G-statistics run (>= ZX + ZR - 1)
   constexpr int NS4 = (NSR + 3) / 4;
-  const ZnccGeom gm = zncc_geom(P, D);
+  const ZnccGeom gm = zncc_geom(P, D, ZTX);
   extern __shared__ __align__(16) float zsm[];
   float* Fs = zsm;                                   // [NRING][FC]    F image rows
   float* Gs = Fs + gm.NRING * gm.FC;                 // [NRING][GROW]  oriented G image rows
@@ -245,7 +250,11 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
   auto orient_s = [&](int c) { return TAR ? c : gm.RS - c; };
 
   // ---- row streaming (loads land raw in registers, converted one iteration later) ----
-  constexpr int NPI = 2, NPS = 4;   // image / statistics elements per thread per row
+  // image / statistics elements per thread per row (upper bounds over P <= 7 and the
+  // D this CTA width serves: 64 for ZTX = 64, 16 for ZT_SMALL)
+  constexpr int DMAX = ZTX == 64 ? 64 : 16;
+  constexpr int NPI = (2 * ZTX + 4 * 7 + DMAX + 32 + 127) / 128;
+  constexpr int NPS = (4 * ZTX + 2 * DMAX + 40 + 127) / 128;
   uint32_t pi_[NPI], ps_[NPS];
   const int NIMG = gm.FC + gm.GC, NSTAT = 2 * ZTX + 2 * gm.SGC;
   auto fetch = [&](int t_img, int y_st) {
@@ -478,15 +487,31 @@ __global__ void RSR_ZNCC_BOUNDS k_zncc(int H, int W, int d_lo, int D, int Dst, i
 
 // Both volumes in one launch (frames [0, B) -> reference, [B, 2B) -> target): one
 // grid twice as long, so the two halves fill each other's last wave.
-template <int P>
-__global__ void RSR_ZNCC_BOUNDS k_zncc_pair(int B, int H, int W, int d_lo, int D, int Dst, int koff,
+// the wide small-D CTA holds more prefetch registers: two CTAs per SM at most
+template <int P, int ZT>
+__global__ void __launch_bounds__(128, (ZT == ZTX ? (P <= 3 ? 3 : (P <= 5 ? 2 : 1)) : (P <= 5 ? 2 : 1)))
+    k_zncc_pair(int B, int H, int W, int d_lo, int D, int Dst, int koff,
                                             const uint8_t* ref, const uint8_t* warped, const int32_t* SLg,
                                             const float* invLg, const int32_t* SWg, const float* invWg,
                                             float* vol_ref, float* vol_tar) {
   if ((int)blockIdx.z < B)
-    zncc_cta<P, false>(blockIdx.z, H, W, d_lo, D, Dst, koff, ref, warped, SLg, invLg, SWg, invWg, vol_ref);
+    zncc_cta<P, false, ZT>(blockIdx.z, H, W, d_lo, D, Dst, koff, ref, warped, SLg, invLg, SWg, invWg, vol_ref);
   else
-    zncc_cta<P, true>(blockIdx.z - B, H, W, d_lo, D, Dst, koff, ref, warped, SLg, invLg, SWg, invWg, vol_tar);
+    zncc_cta<P, true, ZT>(blockIdx.z - B, H, W, d_lo, D, Dst, koff, ref, warped, SLg, invLg, SWg, invWg, vol_tar);
+}
+
+template <int P, int ZT>
+static cudaError_t zncc_pair_launch_zt(int B, int H, int W, int d_lo, int D, int Dst, int koff, const uint8_t* ref,
+                                       const uint8_t* warped, const int32_t* SL, const float* invL,
+                                       const int32_t* SW, const float* invW, float* vol_ref, float* vol_tar,
+                                       cudaStream_t st) {
+  const size_t smem = zncc_smem(P, D, ZT);
+  auto kern = k_zncc_pair<P, ZT>;
+  cudaError_t e = smem_optin((const void*)kern, smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((W + ZT - 1) / ZT, (H + ZBY - 1) / ZBY, 2 * B);
+  kern<<<grid, 128, smem, st>>>(B, H, W, d_lo, D, Dst, koff, ref, warped, SL, invL, SW, invW, vol_ref, vol_tar);
+  return cudaGetLastError();
 }
 
 template <int P>
@@ -494,13 +519,11 @@ static cudaError_t zncc_pair_launch_t(int B, int H, int W, int d_lo, int D, int 
                                       const uint8_t* warped, const int32_t* SL, const float* invL,
                                       const int32_t* SW, const float* invW, float* vol_ref, float* vol_tar,
                                       cudaStream_t st) {
-  const size_t smem = zncc_smem(P, D);
-  auto kern = k_zncc_pair<P>;
-  cudaError_t e = smem_optin((const void*)kern, smem);
-  if (e != cudaSuccess) return e;
-  dim3 grid((W + ZTX - 1) / ZTX, (H + ZBY - 1) / ZBY, 2 * B);
-  kern<<<grid, 128, smem, st>>>(B, H, W, d_lo, D, Dst, koff, ref, warped, SL, invL, SW, invW, vol_ref, vol_tar);
-  return cudaGetLastError();
+  if (zncc_cta_cols(D) == ZT_SMALL)
+    return zncc_pair_launch_zt<P, ZT_SMALL>(B, H, W, d_lo, D, Dst, koff, ref, warped, SL, invL, SW, invW,
+                                            vol_ref, vol_tar, st);
+  return zncc_pair_launch_zt<P, ZTX>(B, H, W, d_lo, D, Dst, koff, ref, warped, SL, invL, SW, invW, vol_ref,
+                                     vol_tar, st);
 }
 
 template <int P, bool TAR>

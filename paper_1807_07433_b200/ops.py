@@ -370,3 +370,40 @@ def rsr_disparity_linear(agg_ref, agg_tar, shift, d_lo, d_hi, lrc_tol, subpixel=
         RsrShape(B, H, W), RsrDispParams(d_lo, d_hi, lrc_tol, 1 if subpixel else 0), _ptr(agg_ref),
         _ptr(agg_tar), _ptr(shift), _ptr(disparity), _ptr(wta_ref), _ptr(wta_tar), _stream()))
     return disparity, wta_ref, wta_tar
+
+
+# --------------------------------------------------------------------------- #
+# Fused, volume-free matching (NEXT row f1; include/rsr.h rsr_match)
+# --------------------------------------------------------------------------- #
+def rsr_match(ref, warped, valid, shift, rho_block, d_lo, d_hi, rho, gamma_d, gamma_r, lrc_tol, subpixel=True,
+              disparity=None, wta_ref=None, wta_tar=None, with_wta=False, workspace=None):
+    """Steps 2-5a fused (D <= 8): disparity float32 [B,H,W] (+ wta maps), bitwise equal to
+    rsr_cost_volume -> rsr_aggregate x2 -> rsr_disparity."""
+    ref, s = _bhw(ref)
+    B, H, W = ref.shape
+    warped, _ = _bhw(warped)
+    valid, _ = _bhw(valid)
+    _expect(ref, torch.uint8, (B, H, W), "ref")
+    _expect(warped, torch.uint8, (B, H, W), "warped")
+    _expect(valid, torch.uint8, (B, H, W), "valid")
+    shift = shift.reshape(B, H)
+    _expect(shift, torch.int32, (B, H), "shift")
+    dev = ref.device
+    disparity = torch.empty((B, H, W), dtype=torch.float32, device=dev) if disparity is None else disparity
+    if with_wta:
+        wta_ref = torch.empty((B, H, W), dtype=torch.int16, device=dev) if wta_ref is None else wta_ref
+        wta_tar = torch.empty((B, H, W), dtype=torch.int16, device=dev) if wta_tar is None else wta_tar
+    _expect(disparity, torch.float32, (B, H, W), "disparity")
+    _expect(wta_ref, torch.int16, (B, H, W), "wta_ref")
+    _expect(wta_tar, torch.int16, (B, H, W), "wta_tar")
+    nbytes = cost_workspace_bytes(B, H, W)
+    if workspace is None:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    if workspace.dtype != torch.uint8 or workspace.dim() != 1 or workspace.numel() < nbytes:
+        raise ValueError(f"rsr: workspace must be a uint8 vector of >= {nbytes} bytes")
+    check("rsr_match", lib().rsr_match(
+        s, RsrCostParams(rho_block, d_lo, d_hi), RsrAggParams(rho, float(gamma_d), float(gamma_r), 1),
+        RsrDispParams(d_lo, d_hi, lrc_tol, 1 if subpixel else 0), _ptr(ref), _ptr(warped), _ptr(valid),
+        _ptr(shift), _ptr(disparity), _ptr(wta_ref), _ptr(wta_tar), _ptr(workspace), workspace.numel(),
+        _stream()))
+    return disparity, wta_ref, wta_tar
