@@ -100,23 +100,21 @@ __global__ void __launch_bounds__(SM_TX, 2) k_aggregate_small(const SmallArgs A)
   int partial = A.nan_map == nullptr ? 1 : 0;
   if (!partial) {
     const int fw = CX, fh = (yb - ya) + 2 * RHO;
-    for (int e = tid; e < fw * fh; e += SM_TX) {
-      const int yy = ya - RHO + e / fw, xx = x0 - RHO + e % fw;
-      if (yy >= 0 && yy < A.H && xx >= 0 && xx < A.W && (A.nan_map[pix0 + (size_t)yy * A.W + xx] & 3) == 3)
-        partial = 1;
+    constexpr int UNR = 8;   // independent loads in flight per thread
+    for (int e0 = tid; e0 < fw * fh; e0 += UNR * SM_TX) {
+      int m[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; u++) {
+        const int e = e0 + u * SM_TX;
+        const int yy = ya - RHO + e / fw, xx = x0 - RHO + e % fw;
+        m[u] = (e < fw * fh && yy >= 0 && yy < A.H && xx >= 0 && xx < A.W)
+                   ? (int)__ldg(A.nan_map + pix0 + (size_t)yy * A.W + xx) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; u++) partial |= (m[u] & 3) == 3;
     }
   }
   const bool clean = !__syncthreads_or(partial);
-
-  // pixel class from nan_map: skipped (outside the image or all k NaN) or not
-  auto skipped = [&](int yy, int xx) {
-    if (yy < 0 || yy >= A.H || xx < 0 || xx >= A.W) return true;
-    return A.nan_map != nullptr && (A.nan_map[pix0 + (size_t)yy * A.W + xx] & 3) == 1;
-  };
-  auto guide_code = [&](int yy, int xx, bool centre) {
-    if (skipped(yy, xx)) return centre ? SM_SKIPP : SM_SKIPQ;
-    return (int)A.guide[pix0 + (size_t)yy * A.W + xx];
-  };
 
   const int NR = (yb - ya) + 2 * RHO;   // input rows ya - RHO .. yb + RHO - 1
   // the row loop, specialised on the path (clean / general) so each instantiation
@@ -127,50 +125,74 @@ __global__ void __launch_bounds__(SM_TX, 2) k_aggregate_small(const SmallArgs A)
   for (int pass = 0; pass < npass; pass++) {
     // staged values per column: clean: costs k0..k0+7 (NaN-free: skipped pixels and
     // k >= D give 0); general pass h: (C0, V) pairs of k0 + 4h .. k0 + 4h + 3
-    auto fetch_row = [&](int i, float (&v)[2][SM_KD], int (&gv)[2]) {
+    // Row staging without data-dependent control flow before the math: every load of
+    // row i + 1 (nan_map byte, guide, costs) is issued unconditionally (in-image
+    // predicate only) at the start of row i and resolved (skip -> weight 0, cost 0)
+    // when committed after the math, so the global-load latency hides behind the row.
+    auto fetch_row = [&](int i, float (&v)[2][SM_KD], int (&gv)[2], int (&nm)[2]) {
       const int yy = ya - RHO + i;
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         const int c = tid + h * SM_TX;
-        gv[h] = 0;
-#pragma unroll
-        for (int q = 0; q < SM_KD; q++) v[h][q] = 0.f;
-        if (c >= CX) continue;
         const int xx = x0 - RHO + c;
-        gv[h] = guide_code(yy, xx, false);
-        if (gv[h] == SM_SKIPQ) continue;       // weight 0; cost (0) or pair (0, 0)
-        const float* src = A.vol + (pix0 + (size_t)yy * A.W + xx) * A.D + k0;
+        const bool in = c < CX && yy >= 0 && yy < A.H && xx >= 0 && xx < A.W;
+        const size_t g = pix0 + (size_t)yy * A.W + xx;
+        nm[h] = in ? (A.nan_map ? (int)A.nan_map[g] : 2) : 1;
+        gv[h] = in ? (int)A.guide[g] : 0;
+        const float* src = A.vol + g * A.D + k0;
         if (CLEAN && ks_eff == SM_KD && (A.D & 3) == 0) {
-          const float4 t0 = __ldg(reinterpret_cast<const float4*>(src));
-          const float4 t1 = __ldg(reinterpret_cast<const float4*>(src + 4));
+          float4 t0 = make_float4(0.f, 0.f, 0.f, 0.f), t1 = t0;
+          if (in) {
+            t0 = __ldg(reinterpret_cast<const float4*>(src));
+            t1 = __ldg(reinterpret_cast<const float4*>(src + 4));
+          }
           v[h][0] = t0.x; v[h][1] = t0.y; v[h][2] = t0.z; v[h][3] = t0.w;
           v[h][4] = t1.x; v[h][5] = t1.y; v[h][6] = t1.z; v[h][7] = t1.w;
         } else if (CLEAN) {
 #pragma unroll
-          for (int q = 0; q < SM_KD; q++) v[h][q] = q < ks_eff ? __ldg(src + q) : 0.f;
+          for (int q = 0; q < SM_KD; q++) v[h][q] = (in && q < ks_eff) ? __ldg(src + q) : 0.f;
         } else {
 #pragma unroll
           for (int q = 0; q < 4; q++) {
             const int k = 4 * pass + q;
-            const float cv = k < ks_eff ? __ldg(src + k) : qnan();
-            const bool ok = !(cv != cv);
-            v[h][2 * q] = ok ? cv : 0.f;
-            v[h][2 * q + 1] = ok ? 1.f : 0.f;
+            v[h][q] = (in && k < ks_eff) ? __ldg(src + k) : qnan();
           }
         }
       }
     };
-    auto commit_row = [&](int i, const float (&v)[2][SM_KD], const int (&gv)[2]) {
+    auto commit_row = [&](int i, const float (&v)[2][SM_KD], const int (&gv)[2], const int (&nm)[2]) {
       const int st = i & 1;
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         const int c = tid + h * SM_TX;
         if (c >= CX) continue;
+        const bool skip = (nm[h] & 3) == 1;      // outside the image or every k NaN
+        float o[SM_KD];
+        if (CLEAN) {
+#pragma unroll
+          for (int q = 0; q < SM_KD; q++) o[q] = skip ? 0.f : v[h][q];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const float cv = v[h][q];
+            const bool ok = !skip && !(cv != cv);
+            o[2 * q] = ok ? cv : 0.f;
+            o[2 * q + 1] = ok ? 1.f : 0.f;
+          }
+        }
         float4* d = reinterpret_cast<float4*>(cost + ((size_t)st * CX + c) * SM_KD);
-        d[0] = make_float4(v[h][0], v[h][1], v[h][2], v[h][3]);
-        d[1] = make_float4(v[h][4], v[h][5], v[h][6], v[h][7]);
-        grow[st * CX + c] = gv[h];
+        d[0] = make_float4(o[0], o[1], o[2], o[3]);
+        d[1] = make_float4(o[4], o[5], o[6], o[7]);
+        grow[st * CX + c] = skip ? SM_SKIPQ : gv[h];
       }
+    };
+    // centre guide code (skipped centre: SM_SKIPP) with unconditional loads
+    auto centre_code = [&](int yy) {
+      const bool in = yy >= 0 && yy < A.H && x < A.W;
+      const size_t g = pix0 + (size_t)yy * A.W + x;
+      const int nmv = in ? (A.nan_map ? (int)A.nan_map[g] : 2) : 1;
+      const int gv = in ? (int)A.guide[g] : 0;
+      return (nmv & 3) == 1 ? SM_SKIPP : gv;
     };
 
     float2 acc[NT][4];
@@ -181,49 +203,67 @@ __global__ void __launch_bounds__(SM_TX, 2) k_aggregate_small(const SmallArgs A)
 #pragma unroll
       for (int q = 0; q < 4; q++) acc[a][q] = make_float2(0.f, 0.f);
       den[a] = 0.f;
-      gp[a] = guide_code(ya - 2 * RHO + a, x, true);   // age a at input row 0: output row ya - 2 rho + a
+      gp[a] = centre_code(ya - 2 * RHO + a);   // age a at input row 0: output row ya - 2 rho + a
     }
-    // clean rows of a whole 8-disparity slab (16-byte aligned): staged by cp.async straight
-    // into shared memory; other rows go through registers (fetch_row / commit_row)
+    // clean rows of a whole 8-disparity slab (16-byte aligned): costs staged by cp.async
+    // straight into shared memory (skipped pixels zeroed at commit); the nan_map byte and
+    // the guide go through registers
     const bool async_rows = CLEAN && ks_eff == SM_KD && (A.D & 3) == 0;
-    auto stage_async = [&](int i) {
+    auto stage_async = [&](int i, int (&gv)[2], int (&nm)[2]) {
       const int yy = ya - RHO + i;
       const int st = i & 1;
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         const int c = tid + h * SM_TX;
-        if (c >= CX) continue;
         const int xx = x0 - RHO + c;
-        const int gv = guide_code(yy, xx, false);
-        grow[st * CX + c] = gv;
-        float* d = cost + ((size_t)st * CX + c) * SM_KD;
-        if (gv == SM_SKIPQ) {
-          reinterpret_cast<float4*>(d)[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-          reinterpret_cast<float4*>(d)[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        } else {
-          const float* src = A.vol + (pix0 + (size_t)yy * A.W + xx) * A.D + k0;
+        const bool in = c < CX && yy >= 0 && yy < A.H && xx >= 0 && xx < A.W;
+        const size_t g = pix0 + (size_t)yy * A.W + xx;
+        nm[h] = in ? (A.nan_map ? (int)A.nan_map[g] : 2) : 1;
+        gv[h] = in ? (int)A.guide[g] : 0;
+        if (in) {
+          float* d = cost + ((size_t)st * CX + c) * SM_KD;
+          const float* src = A.vol + g * A.D + k0;
           cp_async16(d, src);
           cp_async16(d + 4, src + 4);
         }
       }
       cp_async_commit();
     };
-    float pv[2][SM_KD];
-    int pg[2];
-    if (async_rows) {
-      stage_async(0);
+    auto commit_async = [&](int i, const int (&gv)[2], const int (&nm)[2]) {
       cp_async_wait_all();
+      const int st = i & 1;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int c = tid + h * SM_TX;
+        if (c >= CX) continue;
+        const bool skip = (nm[h] & 3) == 1;
+        if (skip) {
+          float4* d = reinterpret_cast<float4*>(cost + ((size_t)st * CX + c) * SM_KD);
+          d[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+          d[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        grow[st * CX + c] = skip ? SM_SKIPQ : gv[h];
+      }
+    };
+    float pv[2][SM_KD];
+    int pg[2], pn[2];
+    if (async_rows) {
+      stage_async(0, pg, pn);
+      commit_async(0, pg, pn);
     } else {
-      fetch_row(0, pv, pg);
-      commit_row(0, pv, pg);
+      fetch_row(0, pv, pg, pn);
+      commit_row(0, pv, pg, pn);
     }
     __syncthreads();
     for (int i = 0; i < NR; i++) {
       // the next row lands in the other stage (last read in iteration i - 1) during the math
       if (i + 1 < NR) {
-        if (async_rows) stage_async(i + 1);
-        else fetch_row(i + 1, pv, pg);
+        if (async_rows) stage_async(i + 1, pg, pn);
+        else fetch_row(i + 1, pv, pg, pn);
       }
+      // centre guide code of the output row entering at the end of this row: loaded now,
+      // consumed after the math (its global-load latency hidden behind the row)
+      const int gp_next = centre_code(ya - 2 * RHO + i + NT);
       const int st = i & 1;
       const float* crow = cost + ((size_t)st * CX + tid) * SM_KD;
       const int* gr = grow + st * CX + tid;
@@ -297,10 +337,10 @@ __global__ void __launch_bounds__(SM_TX, 2) k_aggregate_small(const SmallArgs A)
       }
 #pragma unroll
       for (int a = 0; a + 1 < NT; a++) gp[a] = gp[a + 1];
-      gp[NT - 1] = guide_code(ya - 2 * RHO + i + NT, x, true);
+      gp[NT - 1] = gp_next;
       if (i + 1 < NR) {
-        if (async_rows) cp_async_wait_all();
-        else commit_row(i + 1, pv, pg);
+        if (async_rows) commit_async(i + 1, pg, pn);
+        else commit_row(i + 1, pv, pg, pn);
       }
       __syncthreads();
     }

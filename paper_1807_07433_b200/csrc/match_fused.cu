@@ -8,7 +8,8 @@
 // A CTA owns a 120-column strip of reference pixels and the 128 target-view
 // columns their left-right check reads ([x0 - d_hi, x0 - d_hi + 128)), and slides
 // down a chunk of rows one input row at a time:
-//   N1  image rows (ring of 2 varrho + 2) and the block statistics of the row;
+//   N1  image rows (ring of 2 varrho + 2), the block statistics and guide bytes of
+//       the row, prefetched into registers during the previous row's aggregation;
 //   N2  exact vertical NCC dot sums (sliding, fp32 integers < 2^24);
 //   N3  horizontal sums and the normalisation of K2 (zncc.cu: error-free
 //       products, (num * inv_L) * inv_W, clamp) -> the reference-volume cost row
@@ -79,7 +80,8 @@ struct MatchGeom {
   static constexpr size_t o_g = o_st + 4 * (2 * CW + 2 * (CW + MF_KD));
   static constexpr size_t o_m = o_g + 4 * NRG * (RC + TC);
   static constexpr size_t o_kr = o_m + 4 * NRG * (RC + TC);
-  static constexpr size_t bytes = o_kr + 4 * MF_TXT;
+  static constexpr size_t o_gb = o_kr + 4 * MF_TXT;           // guide bytes of the next row [RC + TC]
+  static constexpr size_t bytes = o_gb + 4 * (RC + TC);
 };
 
 template <int RHO>
@@ -99,6 +101,7 @@ __global__ void __launch_bounds__(MF_THREADS, 1) k_match_fused(const MatchArgs A
   int* gring = reinterpret_cast<int*>(mf_smem + G::o_g);
   int* mring = reinterpret_cast<int*>(mf_smem + G::o_m);
   int* krow = reinterpret_cast<int*>(mf_smem + G::o_kr);
+  int* gbuf = reinterpret_cast<int*>(mf_smem + G::o_gb);
   const int tid = threadIdx.x, lane = tid & 31;
 
   const int H = A.H, W = A.W, D = A.D, P = A.P;
@@ -169,36 +172,101 @@ __global__ void __launch_bounds__(MF_THREADS, 1) k_match_fused(const MatchArgs A
 #pragma unroll
   for (int u = 0; u < NVS; u++) vs[u] = 0.f;
 
-  // prologue: image rows (ya - RHO) - P .. (ya - RHO) + P
-  for (int t = -P; t <= P; t++) load_image_row(ya - RHO + t);
+  // ---- row inputs, prefetched one row ahead into registers (issued before row i's
+  // aggregation, committed to shared memory at the start of row i + 1): the image row
+  // entering the NCC window, the block statistics and the guide bytes of the row ----
+  const int NIMG = VSW + GW;                        // L then W entries
+  const int NSTA = 2 * CW + 2 * (CW + D - 1);       // S_L, inv_L, S_W, inv_W
+  const int NGUI = RC + TC;
+  constexpr int PFI = (G::VSW + G::GW + MF_THREADS - 1) / MF_THREADS;
+  constexpr int PFS = (4 * G::CW + 2 * MF_KD + MF_THREADS - 1) / MF_THREADS;
+  constexpr int PFG = (RC + TC + MF_THREADS - 1) / MF_THREADS;
+  uint32_t pfi[PFI], pfs[PFS], pfg[PFG];
+  auto fetch_rows = [&](int yimg, int ystat) {   // yimg < -1000: no image row
+#pragma unroll
+    for (int u = 0; u < PFI; u++) {
+      const int e = tid + u * MF_THREADS;
+      uint32_t v = 0u;
+      if (e < NIMG && yimg >= 0 && yimg < H) {
+        const bool isL = e < VSW;
+        const int xx = isL ? xcl0 - P + e : gw0 + (e - VSW);
+        if (xx >= 0 && xx < W) v = isL ? A.ref[pix0 + (size_t)yimg * W + xx] : A.warped[pix0 + (size_t)yimg * W + xx];
+      }
+      pfi[u] = v;
+    }
+    const bool rin = ystat >= 0 && ystat < H;
+#pragma unroll
+    for (int u = 0; u < PFS; u++) {
+      const int e = tid + u * MF_THREADS;
+      uint32_t v = 0u;
+      if (e < NSTA) {
+        // [0, CW) S_L, [CW, 2 CW) inv_L, [2 CW, 3 CW + D - 1) S_W, then inv_W
+        const bool isL = e < 2 * CW;
+        const int ee = isL ? e : e - 2 * CW;
+        const int per = isL ? CW : CW + D - 1;
+        const bool isInv = ee >= per;
+        const int xx = (isL ? xcl0 : xcl0 - d_hi) + (isInv ? ee - per : ee);
+        const bool in = rin && xx >= 0 && xx < W;
+        const size_t g = pix0 + (size_t)ystat * W + xx;
+        if (isInv) v = in ? __float_as_uint(isL ? A.iL[g] : A.iW[g]) : 0x7fffffffu;
+        else v = in ? __float_as_uint((float)(isL ? A.SL[g] : A.SW[g])) : 0u;
+      }
+      pfs[u] = v;
+    }
+#pragma unroll
+    for (int u = 0; u < PFG; u++) {
+      const int e = tid + u * MF_THREADS;
+      uint32_t v = 0u;
+      if (e < NGUI && rin) {
+        const bool tar = e >= RC;
+        const int xx = (tar ? xt0 : x0) - RHO + (tar ? e - RC : e);
+        if (xx >= 0 && xx < W) v = (tar ? A.warped : A.ref)[pix0 + (size_t)ystat * W + xx];
+      }
+      pfg[u] = v;
+    }
+  };
+  auto commit_rows = [&](int yimg) {
+    if (yimg > -1000) {
+      const int slot = ((yimg % NRI) + NRI) % NRI;
+#pragma unroll
+      for (int u = 0; u < PFI; u++) {
+        const int e = tid + u * MF_THREADS;
+        if (e < VSW) Lr[slot * G::VSW + e] = (float)pfi[u];
+        else if (e < NIMG) Wr[slot * G::GW + (e - VSW)] = (float)pfi[u];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PFS; u++) {
+      const int e = tid + u * MF_THREADS;
+      if (e < NSTA) st[e] = __uint_as_float(pfs[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < PFG; u++) {
+      const int e = tid + u * MF_THREADS;
+      if (e < NGUI) gbuf[e] = (int)pfg[u];
+    }
+  };
+
+  // prologue: image rows (ya - RHO) - P .. (ya - RHO) + P, statistics and guide of row 0
+  for (int t = -P; t < P; t++) load_image_row(ya - RHO + t);
+  fetch_rows(ya - RHO + P, ya - RHO);
+  commit_rows(ya - RHO + P);
   __syncthreads();
 
   for (int i = 0; i < NR; i++) {
     const int yin = ya - RHO + i;
-    // ---- N1: new image row, statistics of row yin ----
-    if (i > 0) load_image_row(yin + P);
+    // guide value of the output row entering as the oldest age at the end of this row:
+    // loaded now, used after the row (latency hidden)
+    int gp_next;
     {
-      const bool rin = yin >= 0 && yin < H;
-      float* sl = st;                  // S_L [CW]
-      float* il = st + CW;             // inv_L [CW]
-      float* sw = st + 2 * CW;         // S_W [CW + D - 1], column xcl0 - d_hi + c
-      float* iw = sw + (CW + D - 1);   // inv_W
-      for (int c = tid; c < CW; c += MF_THREADS) {
-        const int xx = xcl0 + c;
-        const bool in = rin && xx >= 0 && xx < W;
-        const size_t g = pix0 + (size_t)yin * W + xx;
-        sl[c] = in ? (float)A.SL[g] : 0.f;
-        il[c] = in ? A.iL[g] : qnan();
-      }
-      for (int c = tid; c < CW + D - 1; c += MF_THREADS) {
-        const int xx = xcl0 - d_hi + c;
-        const bool in = rin && xx >= 0 && xx < W;
-        const size_t g = pix0 + (size_t)yin * W + xx;
-        sw[c] = in ? (float)A.SW[g] : 0.f;
-        iw[c] = in ? A.iW[g] : qnan();
-      }
+      const int yn = yin + RHO + 1;
+      gp_next = (yn >= 0 && yn < H && xg >= 0 && xg < W) ? (int)guide[pix0 + (size_t)yn * W + xg] : 0;
     }
-    __syncthreads();
+    // ---- N1: commit the prefetched image row yin + P, statistics and guide of row yin ----
+    if (i > 0) {
+      commit_rows(yin + P);
+      __syncthreads();
+    }
     // ---- N2: exact vertical dot sums over rows yin - P .. yin + P ----
 #pragma unroll
     for (int u = 0; u < NVS; u++) {
@@ -265,12 +333,13 @@ __global__ void __launch_bounds__(MF_THREADS, 1) k_match_fused(const MatchArgs A
       float* d = (tar ? T0 : R0) + cc * MF_KD;
 #pragma unroll
       for (int k = 0; k < MF_KD; k++) d[k] = (skip || (nanm >> k & 1)) ? 0.f : v[k];
-      const uint8_t* gimg = tar ? A.warped : A.ref;
-      gring[gslot * (RC + TC) + c] = skip ? MF_SKIPQ : (int)gimg[pix0 + (size_t)yin * W + xx];
+      gring[gslot * (RC + TC) + c] = skip ? MF_SKIPQ : gbuf[c];
       // NaN bits (k < D) of a non-skipped pixel (bit 8 marks a skipped one)
       mring[gslot * (RC + TC) + c] = skip ? 0x100 : (nanm & ((1 << D) - 1));
     }
     __syncthreads();
+    // next row's inputs in flight during the aggregation
+    if (i + 1 < NR) fetch_rows(yin + 1 + P, yin + 1);
     // ---- A: sliding aggregation of the thread's column ----
     const int gbase = gslot * (RC + TC) + (is_tar ? RC + col : col);
     const float* crow = (is_tar ? T0 : R0) + col * MF_KD;
@@ -379,12 +448,9 @@ __global__ void __launch_bounds__(MF_THREADS, 1) k_match_fused(const MatchArgs A
       vor[a] = vor[a + 1];
       cen[a] = cen[a + 1];
     }
-    {
-      const int yn = yin + RHO + 1;   // output row entering as the oldest age at input row i + 1
-      gp[NT - 1] = (yn >= 0 && yn < H && xg >= 0 && xg < W) ? (int)guide[pix0 + (size_t)yn * W + xg] : 0;
-      vor[NT - 1] = 0;
-      cen[NT - 1] = 0xFF;
-    }
+    gp[NT - 1] = gp_next;   // output row yin + RHO + 1 enters as the oldest age
+    vor[NT - 1] = 0;
+    cen[NT - 1] = 0xFF;
     __syncthreads();   // k_R of row y in shared memory
     if (out_row && !is_tar && col < MF_TXR && xg < W) {
       const size_t o = pix0 + (size_t)y * W + xg;

@@ -19,6 +19,7 @@
 // Output layout [B][H][W][D]: the thread's 8 disparities of one pixel are 32
 // contiguous bytes (two 16-byte stores); 8 lanes cover one pixel's 64 k.
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -201,14 +202,24 @@ __host__ __device__ inline ZnccGeom zncc_geom(int p, int D, int ZTX = rsr::ZTX) 
   return g;
 }
 
-__host__ __device__ inline size_t zncc_smem(int p, int D, int ZTX = rsr::ZTX) {
+__host__ __device__ inline size_t zncc_smem(int p, int D, int ZTX = rsr::ZTX, bool shear = false) {
   const ZnccGeom g = zncc_geom(p, D, ZTX);
-  // ring: F rows, oriented G rows x2; statistics double buffer: sF, iF, sG x2, iG x2
-  return sizeof(float) * ((size_t)g.NRING * (g.FC + 2 * g.GROW) + 2 * (2 * ZTX + 4 * (size_t)g.SROW2));
+  // ring: F rows, oriented G rows x2; statistics double buffer: sF, iF, sG x2, iG x2;
+  // SHEAR: the reference tile of the row [ZTX][ZT_STR]
+  return sizeof(float) * ((size_t)g.NRING * (g.FC + 2 * g.GROW) + 2 * (2 * ZTX + 4 * (size_t)g.SROW2) +
+                          (shear ? (size_t)ZTX * 68 : 0));
 }
 
 // One CTA of the volume kernel for frame b (the kernels below pick b and TAR).
-template <int P, bool TAR, int ZTX = rsr::ZTX>
+// SHEAR (reference CTAs only): the target volume is written from the reference
+// tile by the shear identity of P:106, C_R[v][u'][k] = C_L[v][u' + d_lo + k][k]
+// (NaN where u' + d_lo + k leaves the image): the row's reference costs are staged
+// in a shared tile and copied out as contiguous per-pixel k-runs.  Bitwise the
+// values the target CTAs would compute (same operations, see below), with half the
+// NCC work.
+constexpr int ZT_STR = 68;   // shared tile row stride (floats): conflict-free diagonal reads
+
+template <int P, bool TAR, int ZTX = rsr::ZTX, bool SHEAR = false>
 __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, int Dst, int koff,
                                               const uint8_t* __restrict__ ref,
                                               const uint8_t* __restrict__ warped,
@@ -216,7 +227,9 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
                                               const float* __restrict__ invLg,
                                               const int32_t* __restrict__ SWg,
                                               const float* __restrict__ invWg,
-                                              float* __restrict__ vol) {
+                                              float* __restrict__ vol,
+                                              float* __restrict__ vol_tar = nullptr) {
+  static_assert(!(SHEAR && TAR), "the shear writes the target volume from reference CTAs");
   constexpr int NJ = ZX + 2 * P;          // V columns per thread
   constexpr int NQP = ZR / 2;             // disparity pairs per thread
   constexpr int NGR = NJ + ZR;            // oriented G run loaded per row (>= NJ + ZR - 1)
@@ -230,6 +243,7 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
   float* Gs1 = Gs + gm.NRING * gm.GROW;              // [NRING][GROW]  shifted by one entry
   float* St = Gs1 + gm.NRING * gm.GROW;              // [2][sF ZTX | iF ZTX | sG | sG1 | iG | iG1]
   const int SROW = 2 * ZTX + 4 * gm.SROW2;
+  float* Tt = St + 2 * SROW;                         // SHEAR: [ZTX][ZT_STR] reference costs of the row
 
   const int x0 = blockIdx.x * ZTX, y0 = blockIdx.y * ZBY;
   const int d_hi = d_lo + D - 1;
@@ -456,6 +470,11 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
           const float2 c = TAR ? f2mul(f2mul(num, ig), inf) : f2mul(f2mul(num, inf), ig);
           out[qp] = make_float2(clamp_unit_nan(c.x), clamp_unit_nan(c.y));
         }
+        if (SHEAR) {
+          float* tp = Tt + (ZX * cg + i) * ZT_STR + (r0 - d_lo);
+          reinterpret_cast<float4*>(tp)[0] = make_float4(out[0].x, out[0].y, out[1].x, out[1].y);
+          reinterpret_cast<float4*>(tp)[1] = make_float4(out[2].x, out[2].y, out[3].x, out[3].y);
+        }
         if (u < W) {
           float* dst = vrow + (size_t)u * Dst + (r0 - d_lo);
           if ((Dst & 3) == 0 && (koff & 3) == 0 && nq >= ZR) {
@@ -466,6 +485,27 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
             for (int q = 0; q < ZR; q++)
               if (q < nq) dst[q] = (q & 1) ? out[q >> 1].y : out[q >> 1].x;
           }
+        }
+      }
+    }
+    if (SHEAR) {
+      // C_R[u'][k] = C_L[u' + d_lo + k][k] for the sources in this tile's columns
+      // [x0, x0 + ZTX) (the first / last tile also write the NaN entries whose source
+      // lies left / right of the image): one warp per target pixel u', lanes along k
+      __syncthreads();
+      const int yy = y0 + y;
+      const long long lo_c = x0 == 0 ? -(1LL << 30) : x0;
+      const long long hi_c = x0 + ZTX >= W ? (1LL << 30) : x0 + ZTX - 1;
+      const int ulo = (int)max(0LL, lo_c - d_lo - (D - 1)), uhi = (int)min((long long)W - 1, hi_c - d_lo);
+      float* trow = vol_tar + ((ibase + (size_t)yy * W) * Dst) + koff;
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+      for (int up = ulo + warp; up <= uhi; up += nw) {
+        const int ka = (int)max(0LL, lo_c - d_lo - up), kb = (int)min((long long)D - 1, hi_c - d_lo - up);
+        for (int k = ka + lane; k <= kb; k += 32) {
+          const int sc = up + d_lo + k;
+          float v = qnan();
+          if (sc >= 0 && sc < W) v = Tt[(sc - x0) * ZT_STR + k];
+          trow[(size_t)up * Dst + k] = v;
         }
       }
     }
@@ -514,6 +554,30 @@ static cudaError_t zncc_pair_launch_zt(int B, int H, int W, int d_lo, int D, int
   return cudaGetLastError();
 }
 
+// Both volumes from the reference CTAs alone (SHEAR): grid of B frames
+template <int P>
+__global__ void RSR_ZNCC_BOUNDS k_zncc_shear(int H, int W, int d_lo, int D, int Dst, int koff, const uint8_t* ref,
+                                             const uint8_t* warped, const int32_t* SLg, const float* invLg,
+                                             const int32_t* SWg, const float* invWg, float* vol_ref,
+                                             float* vol_tar) {
+  zncc_cta<P, false, ZTX, true>(blockIdx.z, H, W, d_lo, D, Dst, koff, ref, warped, SLg, invLg, SWg, invWg, vol_ref,
+                                vol_tar);
+}
+
+template <int P>
+static cudaError_t zncc_shear_launch_t(int B, int H, int W, int d_lo, int D, int Dst, int koff, const uint8_t* ref,
+                                       const uint8_t* warped, const int32_t* SL, const float* invL,
+                                       const int32_t* SW, const float* invW, float* vol_ref, float* vol_tar,
+                                       cudaStream_t st) {
+  const size_t smem = zncc_smem(P, D, ZTX, true);
+  auto kern = k_zncc_shear<P>;
+  cudaError_t e = smem_optin((const void*)kern, smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((W + ZTX - 1) / ZTX, (H + ZBY - 1) / ZBY, B);
+  kern<<<grid, 128, smem, st>>>(H, W, d_lo, D, Dst, koff, ref, warped, SL, invL, SW, invW, vol_ref, vol_tar);
+  return cudaGetLastError();
+}
+
 template <int P>
 static cudaError_t zncc_pair_launch_t(int B, int H, int W, int d_lo, int D, int Dst, int koff, const uint8_t* ref,
                                       const uint8_t* warped, const int32_t* SL, const float* invL,
@@ -522,6 +586,13 @@ static cudaError_t zncc_pair_launch_t(int B, int H, int W, int d_lo, int D, int 
   if (zncc_cta_cols(D) == ZT_SMALL)
     return zncc_pair_launch_zt<P, ZT_SMALL>(B, H, W, d_lo, D, Dst, koff, ref, warped, SL, invL, SW, invW,
                                             vol_ref, vol_tar, st);
+  // experiment hook (tools/): RSR_K2_SHEAR=1 writes the target volume by the shear from the
+  // reference CTAs.  Measured slower (c5, 8 frames: 3.51 ms vs 1.64 ms for the pair grid:
+  // the k-runs of a target pixel come from two CTAs, partial 256-byte records), so off
+  const char* e = getenv("RSR_K2_SHEAR");
+  if (e && e[0] == '1')
+    return zncc_shear_launch_t<P>(B, H, W, d_lo, D, Dst, koff, ref, warped, SL, invL, SW, invW, vol_ref, vol_tar,
+                                  st);
   return zncc_pair_launch_zt<P, ZTX>(B, H, W, d_lo, D, Dst, koff, ref, warped, SL, invL, SW, invW, vol_ref,
                                      vol_tar, st);
 }
@@ -599,7 +670,8 @@ __global__ void __launch_bounds__(256) k_nan_maps(int H, int W, int d_lo, int D,
   // [0, H0) and [H0, D) with H0 = roundup8(D) / 2; bits 2 / 3 flag a NaN in each,
   // bit 7 says the half bits are present
   const bool halves = D <= 64;
-  const int H0 = ((D + 7) & ~7) / 2;
+  // the low half [0, H0) is clipped to the D disparities that exist (D <= 3: H0 = 4 > D)
+  const int H0 = min(((D + 7) & ~7) / 2, D);
   for (int u = threadIdx.x; u < W; u += blockDim.x) {
     const bool lok = cL[u + 1] - cL[u] != 0, wok = cW[u + 1] - cW[u] != 0;
     if (nan_ref) {   // k valid iff inv_L(u) and inv_W(u - d_lo - k) finite

@@ -91,7 +91,7 @@ def test_fused_equals_five_calls_edge_cases(rsr, case):
     assert_bitwise(r)
     # and through the five-call path, the oracle's tolerances
     ora = O.run_pipeline(left, right, a, be, cfg)
-    gpu = dict(warped=r["W"][None], mask=r["M"][None], shift=r["S"][None], cost_ref=r["cost_ref"],
+    gpu = dict(warped=r["W"], mask=r["M"], shift=r["S"], cost_ref=r["cost_ref"],
                cost_tar=r["cost_tar"], agg_ref=r["agg_ref"], agg_tar=r["agg_tar"], disparity=r["df"],
                k_ref=r["klf"], k_tar=r["krf"], xyz=np.zeros(r["df"].shape + (3,), np.float32) * np.nan)
     ora["xyz"] = np.full(ora["xyz"].shape, np.nan)

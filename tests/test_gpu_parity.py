@@ -62,6 +62,8 @@ def to_dhw(v):
 
 
 def top_two_gap(agg):
+    if agg.shape[0] < 2:          # D = 1: a single candidate, never a tie
+        return np.full(agg.shape[1:], np.inf)
     a = np.where(np.isnan(agg), -np.inf, agg)
     s = np.sort(a, axis=0)
     with np.errstate(invalid="ignore"):
@@ -140,9 +142,10 @@ def check_warp(gpu, right, ab, b=0):
     assert np.array_equal(gpu["shift"][b].astype(np.int64), So)
 
 
-@pytest.mark.parametrize("name", ["c1", "c2"])
-def test_parity_full_frame(rsr, name):
-    cfg = synth.get_config(name)
+@pytest.mark.parametrize("name,over", [("c1", {}), ("c2", {}), ("c1", {"d_lo": -1, "d_hi": 1}),
+                                       ("c1", {"d_lo": 0, "d_hi": 0})])
+def test_parity_full_frame(rsr, name, over):
+    cfg = synth.get_config(name, **over)
     f = synth.make_frame(cfg)
     gpu = run_gpu(rsr, f.left, f.right, [f.alpha, f.beta], cfg)
     check_warp(gpu, f.right, (f.alpha, f.beta))
@@ -282,6 +285,12 @@ EDGE_CASES = {
     "rho8_D16": (40, 90, -8, 7, 2, 8, 5.0, 12.0, 0.05, 2.0),
     "rho9_D70_two_slabs": (38, 84, -35, 34, 2, 9, 5.0, 12.0, 0.0, 1.0),
     "rho10_D24": (48, 100, -12, 11, 3, 10, 6.0, 12.0, 0.05, 2.0),
+    # D <= 3: the NaN summaries' low half is clipped to D (k_nan_maps); D <= 16 runs the
+    # small-slab K2 / K3 / K4 kernels
+    "D1": (30, 140, 0, 0, 2, 2, 2.0, 10.0, 0.0, 3.0),
+    "D2_rho5": (33, 150, -1, 0, 2, 5, 3.0, 10.0, 0.05, 2.0),
+    "D9_two_small_slabs": (36, 170, -4, 4, 3, 6, 4.0, 12.0, 0.1, 2.0),
+    "D16_rho7": (40, 200, -8, 7, 4, 7, 5.0, 12.0, 0.05, 3.0),
 }
 
 
