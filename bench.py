@@ -498,7 +498,7 @@ def main(argv=None):
         "config": workload_config(cfg, args, world),
         "roofline": {"kernel": "k_aggregate (rsr_aggregate, Eq. 8)", "bound": "alu", "achieved": achieved,
                      "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
-                     "traffic": k3_traffic(),
+                     "traffic": k3_traffic() if cfg.name == "c5" and B == 8 else None,
                      "peak_note": "FP32 FMA: 148 SMs x 128 lanes x 2 flop x 1965 MHz (B200_PROFILING.md unit "
                                   "counts and max clock); measured FFMA-chain peak 71.5 TFLOP/s "
                                   "(profiles/r01_ubench_fp32_lds.jsonl)",

@@ -477,7 +477,7 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
         float* o = A.out + pix * A.D + s.k0 + koff;
         if (CLEAN) {
           // den == 0 exactly when the centre is skipped (all-NaN): 0 * inf = NaN
-          const float inv = __frcp_rn(den);
+          const float inv = rcp_fast(den);
           const float r[8] = {fin[0].x * inv, fin[0].y * inv, fin[1].x * inv, fin[1].y * inv,
                               fin[2].x * inv, fin[2].y * inv, fin[3].x * inv, fin[3].y * inv};
 #pragma unroll
@@ -494,7 +494,7 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
           }
         } else if (hc) {
           // fully valid half: same formula as the clean path (bitwise equal)
-          const float inv = __frcp_rn(den);
+          const float inv = rcp_fast(den);
           const float r[4] = {fin[0].x * inv, fin[0].y * inv, fin[1].x * inv, fin[1].y * inv};
 #pragma unroll
           for (int q = 0; q < 4; q++)
@@ -507,7 +507,7 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
             const int k = s.k0 + koff + q;
             if (k < s.k0 + s.ks_eff) {
               const float c = cv[q];
-              o[q] = (c != c) ? qnan() : fv[2 * q] * __frcp_rn(fv[2 * q + 1]);
+              o[q] = (c != c) ? qnan() : fv[2 * q] * rcp_fast(fv[2 * q + 1]);
             }
           }
         }

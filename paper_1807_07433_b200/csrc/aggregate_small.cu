@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(SM_TX, 2) k_aggregate_small(const SmallArgs A)
       if (y >= ya && x < A.W) {
         float* o = A.out + (pix0 + (size_t)y * A.W + x) * A.D + k0;
         if (CLEAN) {
-          const float inv = __frcp_rn(fden);   // fden == 0 exactly for a skipped centre: NaN
+          const float inv = rcp_fast(fden);   // fden == 0 exactly for a skipped centre: NaN
           const float r[8] = {fin[0].x * inv, fin[0].y * inv, fin[1].x * inv, fin[1].y * inv,
                               fin[2].x * inv, fin[2].y * inv, fin[3].x * inv, fin[3].y * inv};
           if (ks_eff == SM_KD && (A.D & 3) == 0) {
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(SM_TX, 2) k_aggregate_small(const SmallArgs A)
             const int k = 4 * pass + q;
             if (k < ks_eff) {
               const float c = __ldg(cv + k);
-              o[k] = (c != c) ? qnan() : fin[q].x * __frcp_rn(fin[q].y);
+              o[k] = (c != c) ? qnan() : fin[q].x * rcp_fast(fin[q].y);
             }
           }
         }

@@ -78,6 +78,15 @@ RSR_DEVINL float clamp_unit_nan(float c) {
 
 RSR_DEVINL float qnan() { return __int_as_float(0x7fffffff); }
 
+// 1/x on the MUFU pipe (rcp.approx.ftz, <= 1 ulp): the bilateral normalisation of
+// every K3 variant (sliding, small-slab, fused) -- one instruction instead of the
+// IEEE __frcp_rn sequence; 1/0 = +inf, so a zero weight sum still gives NaN.
+RSR_DEVINL float rcp_fast(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Clamp to [-1, 1] keeping NaN (fminf/fmaxf would drop it).
 RSR_DEVINL float clamp_unit_keep_nan(float c) {
   return c > 1.f ? 1.f : (c < -1.f ? -1.f : c);

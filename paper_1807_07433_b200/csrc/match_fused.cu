@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(MF_THREADS, 1) k_match_fused(const MatchArgs A
     int kbest = -1;
     if (out_row) {
       const float f8[8] = {fin[0].x, fin[0].y, fin[1].x, fin[1].y, fin[2].x, fin[2].y, fin[3].x, fin[3].y};
-      const float inv = __frcp_rn(fden);
+      const float inv = rcp_fast(fden);
       const int M = vor[0], cz = cen[0];
       const int gp0 = gp[0];
 #pragma unroll
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(MF_THREADS, 1) k_match_fused(const MatchArgs A
                 dk = fmaf(w, vv, dk);
               }
             }
-            a = f8[k] * __frcp_rn(dk);
+            a = f8[k] * rcp_fast(dk);
           }
         }
         Av[k] = a;

@@ -1,14 +1,18 @@
 #!/bin/bash
-# Round evidence: parity tests, default bench, reference arm, ncu launch list and
-# one full ncu capture of the dominant kernel (K3) - each ncu command only after the
-# same command line exited 0 without ncu.
+# Round evidence: the full -m gpu suite, the default bench (N=1) and through the
+# torchrun spawn path (NCCL group + gather), the reference arm, the ncu launch list
+# and one ncu --set full capture of the dominant kernel (K3) -- each ncu command only
+# after the same command line exited 0 without ncu.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 TAG=${TAG:-ev}
 nvidia-smi --query-gpu=name,driver_version,clocks.sm,clocks.max.sm,power.limit --format=csv > gpurun_out/${TAG}_smi.txt 2>&1
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest_gpu.log
-timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?"
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest_gpu.log
+tail -3 gpurun_out/${TAG}_pytest_gpu.log
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?"
+timeout 600 python bench.py --spawn --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/${TAG}_bench_spawn.json 2> gpurun_out/${TAG}_bench_spawn.err; echo "spawn rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${TAG}_bench_ref.json 2> gpurun_out/${TAG}_bench_ref.err; echo "ref rc=$?"
+for c in c1 c2 c4 cP; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_bench_configs.jsonl 2>> gpurun_out/${TAG}_bench_configs.err; done; echo "configs rc=$?"
 CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launches.log 2>&1; echo "ncu1 rc=$?"
