@@ -262,15 +262,16 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
   float sreg[NAB][NT];   // exp2(kd (dx^2 + dy^2)) for this lane's ages
 #pragma unroll
   for (int n = 0; n < NAB; n++) {
-    const int a = min(((p + 4 * n) % NAB) * 4 + as, NT - 1);
+    const int a = min(n * 4 + as, NT - 1);
 #pragma unroll
     for (int j = 0; j < NT; j++)
       sreg[n][j] = ex2_ftz((float)((j - RHO) * (j - RHO) + (RHO - a) * (RHO - a)) * A.kd);
   }
   const bool cpa = stage_cpasync(A.D, g);
   for (int pass = 0; pass < npass; pass++) {
-    for (int e = p * 32 + lane; e < NT * 32; e += SG_NPROD * 32) dsum[e] = 0.f;
-    asm volatile("bar.sync 1, %0;" ::"r"(SG_NPROD * 32) : "memory");
+    // warp p owns the columns 8p .. 8p + 7 (every age): its running sums are its own
+    for (int e = lane; e < NT * 8; e += 32) dsum[(e >> 3) * 32 + 8 * p + (e & 7)] = 0.f;
+    __syncwarp();
     for (int i = 0; i < NR; i++, it_w++) {
       // cp.async-staged rows: every producer warp issues a share (non-blocking)
       if (cpa || p == 0)
@@ -278,7 +279,8 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
       const int st = it_w % SG_NSW;
       if (it_w >= SG_NSW) mbar_wait_parity(&empty_w[st], ((it_w / SG_NSW) & 1) ^ 1);
       float* wst = w_s + (size_t)st * g.WST;
-      // this warp's items (x-block, age-block) = p + 4 n, n < NAB; all shared-memory
+      // this warp's items: x-block p, age-blocks n < NAB (the running sums of a column
+      // never leave its warp, so no barrier among the producer warps); all shared-memory
       // loads first, then the math, then the stores: the tile, the running sums and
       // the weight stage may alias as far as the compiler knows, so interleaving them
       // would serialise every tap's LDS -> MUFU -> STS chain
@@ -289,8 +291,7 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
       const unsigned short* trs = gt + (i + RHO) * g.CX;   // tap row r
 #pragma unroll
       for (int n = 0; n < NAB; n++) {
-        const int item = p + 4 * n;
-        const int x = (item / NAB) * 8 + xs, a = (item % NAB) * 4 + as;
+        const int x = p * 8 + xs, a = n * 4 + as;
         const int ac = min(a, NT - 1);
         int gp = gt[(i + ac) * g.CX + x + RHO];
         float* slot = dsum + ((i + ac) % NT) * 32 + x;
@@ -326,9 +327,7 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
           }
         }
       }
-      // next tap row as float into the other buffer (its last readers finished before
-      // the previous barrier)
-      asm volatile("bar.sync 1, %0;" ::"r"(SG_NPROD * 32) : "memory");   // row sums handed to the next age
+      __syncwarp();   // row sums handed to the next age (same warp)
       mbar_arrive(&full_w[st]);
     }
   }
