@@ -26,14 +26,16 @@ constexpr int DG = 8;   // lanes per pixel
 // lane sees its disparities in increasing order, so "strictly greater" keeps the
 // first (smallest) index among equal maxima; max(x, NaN) = x skips NaN entries.
 // Per 8 values: 8 FMNMX for the maximum, then the first index equal to it.
+template <int DGT>
 RSR_DEVINL void lane_best(const float* __restrict__ p, int D, int l, bool vec4, float& best, int& kb) {
   best = -INFINITY;
   kb = -1;
-  for (int c0 = 0; c0 < D; c0 += 64) {
+  // chunks of 8 DGT disparities: lane l reads {4l..4l+3} and {4 DGT + 4l..+3}
+  for (int c0 = 0; c0 < D; c0 += 8 * DGT) {
     float v[8];
 #pragma unroll
     for (int h = 0; h < 2; h++) {
-      const int k = c0 + 32 * h + 4 * l;
+      const int k = c0 + 4 * DGT * h + 4 * l;
       if (vec4 && k + 3 < D) {
         const float4 t = __ldg(reinterpret_cast<const float4*>(p + k));
         v[4 * h] = t.x; v[4 * h + 1] = t.y; v[4 * h + 2] = t.z; v[4 * h + 3] = t.w;
@@ -50,15 +52,16 @@ RSR_DEVINL void lane_best(const float* __restrict__ p, int D, int l, bool vec4, 
       int kk = -1;
 #pragma unroll
       for (int q = 7; q >= 0; q--)
-        if (v[q] == m) kk = c0 + 32 * (q >> 2) + 4 * l + (q & 3);
+        if (v[q] == m) kk = c0 + 4 * DGT * (q >> 2) + 4 * l + (q & 3);
       kb = kk;
     }
   }
 }
 
+template <int DGT>
 RSR_DEVINL int group_reduce(float best, int kb) {
 #pragma unroll
-  for (int o = DG / 2; o >= 1; o >>= 1) {
+  for (int o = DGT / 2; o >= 1; o >>= 1) {
     const float ov = __shfl_xor_sync(0xffffffffu, best, o);
     const int ok = __shfl_xor_sync(0xffffffffu, kb, o);
     if (ok >= 0 && (kb < 0 || ov > best || (ov == best && ok < kb))) { best = ov; kb = ok; }
@@ -66,16 +69,10 @@ RSR_DEVINL int group_reduce(float best, int kb) {
   return kb;
 }
 
-RSR_DEVINL int group_argmax(const float* __restrict__ p, int D, int l, bool vec4) {
-  float best;
-  int kb;
-  lane_best(p, D, l, vec4, best, kb);
-  return group_reduce(best, kb);
-}
 
 // ShiftT: int32_t (integer warp, reading 1: d = r_s + s(v) in fp32) or double (the
 // interpolating warp, reading 21: d = fp32(r_s + t_q(v)) with the sum in fp64).
-template <typename ShiftT>
+template <typename ShiftT, int DGT>
 __global__ void __launch_bounds__(256) k_disparity(int H, int W, int d_lo, int D, int tol,
                                                    int subpix, const float* __restrict__ agg_ref,
                                                    const float* __restrict__ agg_tar,
@@ -87,7 +84,7 @@ __global__ void __launch_bounds__(256) k_disparity(int H, int W, int d_lo, int D
   const int v = blockIdx.x, b = blockIdx.y;
   const size_t row = ((size_t)b * H + v) * W;
   const bool vec4 = (D & 3) == 0;
-  const int l = threadIdx.x % DG, g = threadIdx.x / DG, ng = blockDim.x / DG;
+  const int l = threadIdx.x % DGT, g = threadIdx.x / DGT, ng = blockDim.x / DGT;
   const int Wr = (W + 4 * ng - 1) / (4 * ng) * (4 * ng);   // uniform trip count: every lane reaches the shuffles
   // two pixels per group per iteration: four 16-byte loads in flight per lane
   // (measured: 2 beats 1, 4 and 8 -- fewer registers, more resident CTAs)
@@ -98,12 +95,12 @@ __global__ void __launch_bounds__(256) k_disparity(int H, int W, int d_lo, int D
 #pragma unroll
     for (int e = 0; e < UP; e++) {
       const int uu = min(u0 + e * ng, W - 1);
-      lane_best(agg_tar + (row + uu) * D, D, l, vec4, bv[e], bk[e]);
+      lane_best<DGT>(agg_tar + (row + uu) * D, D, l, vec4, bv[e], bk[e]);
     }
 #pragma unroll
     for (int e = 0; e < UP; e++) {
       const int u = u0 + e * ng;
-      const int k = group_reduce(bv[e], bk[e]);
+      const int k = group_reduce<DGT>(bv[e], bk[e]);
       if (l == 0 && u < W) {
         kr_s[u] = (int16_t)k;
         if (wta_tar) wta_tar[row + u] = (int16_t)k;
@@ -118,12 +115,12 @@ __global__ void __launch_bounds__(256) k_disparity(int H, int W, int d_lo, int D
 #pragma unroll
     for (int e = 0; e < UP; e++) {
       const int uu = min(u0 + e * ng, W - 1);
-      lane_best(agg_ref + (row + uu) * D, D, l, vec4, bv[e], bk[e]);
+      lane_best<DGT>(agg_ref + (row + uu) * D, D, l, vec4, bv[e], bk[e]);
     }
 #pragma unroll
     for (int e = 0; e < UP; e++) {
       const int u = u0 + e * ng;
-      const int k = group_reduce(bv[e], bk[e]);
+      const int k = group_reduce<DGT>(bv[e], bk[e]);
       if (l != 0 || u >= W) continue;
       const float* p = agg_ref + (row + u) * D;
       if (wta_ref) wta_ref[row + u] = (int16_t)k;
@@ -218,11 +215,17 @@ static cudaError_t disparity_launch_t(int B, int H, int W, int d_lo, int D, int 
     if (e != cudaSuccess) return e;
     k_disparity_small<ShiftT><<<grid, 256, smem, st>>>(H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, shift, disp,
                                                        wta_ref, wta_tar);
-  } else {
-    const cudaError_t e = smem_optin((const void*)k_disparity<ShiftT>, smem);
+  } else if (D <= 32) {
+    // 16 < D <= 32 (the paper's d_max = 30): 4-lane groups, one 32-wide chunk per pixel
+    const cudaError_t e = smem_optin((const void*)k_disparity<ShiftT, 4>, smem);
     if (e != cudaSuccess) return e;
-    k_disparity<ShiftT><<<grid, 256, smem, st>>>(H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, shift, disp,
-                                                 wta_ref, wta_tar);
+    k_disparity<ShiftT, 4><<<grid, 256, smem, st>>>(H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, shift, disp,
+                                                    wta_ref, wta_tar);
+  } else {
+    const cudaError_t e = smem_optin((const void*)k_disparity<ShiftT, DG>, smem);
+    if (e != cudaSuccess) return e;
+    k_disparity<ShiftT, DG><<<grid, 256, smem, st>>>(H, W, d_lo, D, tol, subpix, agg_ref, agg_tar, shift, disp,
+                                                     wta_ref, wta_tar);
   }
   return cudaGetLastError();
 }

@@ -171,6 +171,9 @@ constexpr int ZTX = 64;   // columns per CTA (16 column groups) for D > 16
 // columns per CTA so that the 128 threads stay busy (one disparity group of 8 per
 // column group of 4: 64 column groups x up to 2 disparity groups).
 constexpr int ZT_SMALL = 256;
+// (a 128-column CTA for 16 < D <= 32 was measured slower at the paper's D = 30:
+// 1.64 vs 1.47 ms per 8 cP frames)
+constexpr int ZT_MID = 128;
 __host__ __device__ constexpr int zncc_cta_cols(int D) { return D <= 16 ? ZT_SMALL : ZTX; }
 constexpr int ZBY = 72;   // output rows per CTA (measured: 72 beats 48/60/80/90/96/144 at c5)
 
@@ -266,7 +269,7 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
   // ---- row streaming (loads land raw in registers, converted one iteration later) ----
   // image / statistics elements per thread per row (upper bounds over P <= 7 and the
   // D this CTA width serves: 64 for ZTX = 64, 16 for ZT_SMALL)
-  constexpr int DMAX = ZTX == 64 ? 64 : 16;
+  constexpr int DMAX = ZTX == 64 ? 64 : (ZTX == ZT_MID ? 32 : 16);
   constexpr int NPI = (2 * ZTX + 4 * 7 + DMAX + 32 + 127) / 128;
   constexpr int NPS = (4 * ZTX + 2 * DMAX + 40 + 127) / 128;
   uint32_t pi_[NPI], ps_[NPS];
@@ -529,7 +532,7 @@ __global__ void RSR_ZNCC_BOUNDS k_zncc(int H, int W, int d_lo, int D, int Dst, i
 // grid twice as long, so the two halves fill each other's last wave.
 // the wide small-D CTA holds more prefetch registers: two CTAs per SM at most
 template <int P, int ZT>
-__global__ void __launch_bounds__(128, (ZT == ZTX ? (P <= 3 ? 3 : (P <= 5 ? 2 : 1)) : (P <= 5 ? 2 : 1)))
+__global__ void __launch_bounds__(128, (ZT != ZT_SMALL ? (P <= 3 ? 3 : (P <= 5 ? 2 : 1)) : (P <= 5 ? 2 : 1)))
     k_zncc_pair(int B, int H, int W, int d_lo, int D, int Dst, int koff,
                                             const uint8_t* ref, const uint8_t* warped, const int32_t* SLg,
                                             const float* invLg, const int32_t* SWg, const float* invWg,
@@ -586,6 +589,9 @@ static cudaError_t zncc_pair_launch_t(int B, int H, int W, int d_lo, int D, int 
   if (zncc_cta_cols(D) == ZT_SMALL)
     return zncc_pair_launch_zt<P, ZT_SMALL>(B, H, W, d_lo, D, Dst, koff, ref, warped, SL, invL, SW, invW,
                                             vol_ref, vol_tar, st);
+  if (zncc_cta_cols(D) == ZT_MID)
+    return zncc_pair_launch_zt<P, ZT_MID>(B, H, W, d_lo, D, Dst, koff, ref, warped, SL, invL, SW, invW,
+                                          vol_ref, vol_tar, st);
   // experiment hook (tools/): RSR_K2_SHEAR=1 writes the target volume by the shear from the
   // reference CTAs.  Measured slower (c5, 8 frames: 3.51 ms vs 1.64 ms for the pair grid:
   // the k-runs of a target pixel come from two CTAs, partial 256-byte records), so off
