@@ -46,23 +46,33 @@ struct SmallArgs {
   float* out;
 };
 
-template <int RHO>
+// SPLIT: two threads per output column (lanes 2c, 2c + 1), the lower holding ages
+// 0 .. RHO and the upper ages RHO + 1 .. 2 RHO (+ one always-zero dummy age), so a
+// thread keeps half the accumulators (~128 registers, four CTAs of 64 columns per SM
+// instead of two of 128: twice the warps to hide the latencies that bound the
+// one-thread-per-column kernel).  The age that crosses from the upper to the lower
+// half at the end of each input row moves by one lane shuffle (exact copies): every
+// accumulation stays in (input row, tap) order, bitwise as before.
+template <int RHO, bool SPLIT>
 struct SmallGeom {
   static constexpr int NT = 2 * RHO + 1;
-  static constexpr int CX = SM_TX + 2 * RHO;       // staged columns per input row
-  static constexpr int STW = NT <= 16 ? 16 : 32;   // spatial table row stride
+  static constexpr int TXC = SPLIT ? 64 : SM_TX;   // output columns per CTA
+  static constexpr int CX = TXC + 2 * RHO;         // staged columns per input row
+  static constexpr int NA = SPLIT ? RHO + 1 : NT;  // ages per thread
+  static constexpr int REP = SPLIT ? 16 : 32;      // range-table copies (lane & (REP - 1))
+  static constexpr int STW = SPLIT ? 16 : (NT <= 16 ? 16 : 32);   // spatial table row stride
   // shared memory (bytes): lut | S | 2 cost rows [CX][8] | 2 guide rows [CX] (int)
   static constexpr size_t off_lut = 0;
-  static constexpr size_t off_s = off_lut + sizeof(float) * SM_LUT * 32;
+  static constexpr size_t off_s = off_lut + sizeof(float) * SM_LUT * REP;
   static constexpr size_t off_cost = off_s + sizeof(float) * NT * STW;
   static constexpr size_t off_guide = off_cost + sizeof(float) * 2 * CX * SM_KD;
   static constexpr size_t bytes = off_guide + sizeof(int) * 2 * CX;
 };
 
-template <int RHO>
-__global__ void __launch_bounds__(SM_TX, 2) k_aggregate_small(const SmallArgs A) {
-  using G = SmallGeom<RHO>;
-  constexpr int NT = G::NT, CX = G::CX;
+template <int RHO, bool SPLIT>
+__global__ void __launch_bounds__(SM_TX, SPLIT ? 4 : 2) k_aggregate_small(const SmallArgs A) {
+  using G = SmallGeom<RHO, SPLIT>;
+  constexpr int NT = G::NT, CX = G::CX, NA = G::NA, TXC = G::TXC, REP = G::REP;
   extern __shared__ __align__(16) unsigned char sm_smem[];
   float* lut = reinterpret_cast<float*>(sm_smem + G::off_lut);
   float* S = reinterpret_cast<float*>(sm_smem + G::off_s);
@@ -71,7 +81,7 @@ __global__ void __launch_bounds__(SM_TX, 2) k_aggregate_small(const SmallArgs A)
   const int tid = threadIdx.x, lane = tid & 31;
 
   // ---- segment: 128 columns x R rows of frame b, disparity slab ----
-  const int nstrip = (A.W + SM_TX - 1) / SM_TX;
+  const int nstrip = (A.W + TXC - 1) / TXC;
   const int nchunk = (A.H + A.R - 1) / A.R;
   int blk = blockIdx.x;
   const int strip = blk % nstrip;
@@ -79,20 +89,24 @@ __global__ void __launch_bounds__(SM_TX, 2) k_aggregate_small(const SmallArgs A)
   const int chunk = blk % nchunk;
   blk /= nchunk;
   const int slab = blk % A.nslab, b = blk / A.nslab;
-  const int x0 = strip * SM_TX, ya = chunk * A.R, yb = min(A.H, ya + A.R);
+  const int x0 = strip * TXC, ya = chunk * A.R, yb = min(A.H, ya + A.R);
   const int k0 = slab * SM_KD, ks_eff = min(SM_KD, A.D - k0);
   const size_t pix0 = (size_t)b * A.H * A.W;
-  const int x = x0 + tid;
+  const int tc = SPLIT ? tid >> 1 : tid;            // the thread's column in the strip
+  const int hf = SPLIT ? (tid & 1) : 0;             // SPLIT: lower (0) / upper (1) ages
+  const int x = x0 + tc;
 
   // ---- tables: range factor exp2(kr dg^2) per lane, spatial factor exp2(kd (dx^2 + dy^2)) ----
-  for (int e = tid; e < SM_LUT * 32; e += SM_TX) {
-    const int dg = e / 32 - 255;
+  for (int e = tid; e < SM_LUT * REP; e += SM_TX) {
+    const int dg = e / REP - 255;
     lut[e] = (dg <= 255) ? ex2_ftz((float)(dg * dg) * A.kr) : 0.f;
   }
   // S[j][a]: tap j (dx = j - RHO), age a = output row y_in - RHO + a (dy = RHO - a);
-  // ages contiguous so four of them are one broadcast LDS.128
+  // ages contiguous so four of them are one broadcast LDS.128.  SPLIT: [j][half][8],
+  // half 1 starting at age RHO + 1 (its dummy age and padding: 0)
   for (int e = tid; e < NT * G::STW; e += SM_TX) {
-    const int j = e / G::STW, a = e % G::STW;
+    const int j = e / G::STW, r = e % G::STW;
+    const int a = SPLIT ? (r >= 8 ? RHO + 1 + (r - 8) : (r < RHO + 1 ? r : NT)) : r;
     S[e] = a < NT ? ex2_ftz((float)((j - RHO) * (j - RHO) + (RHO - a) * (RHO - a)) * A.kd) : 0.f;
   }
 
@@ -195,15 +209,16 @@ __global__ void __launch_bounds__(SM_TX, 2) k_aggregate_small(const SmallArgs A)
       return (nmv & 3) == 1 ? SM_SKIPP : gv;
     };
 
-    float2 acc[NT][4];
-    float den[NT];
-    int gp[NT];   // guide code of the output row of each age (its centre pixel)
+    float2 acc[NA][4];
+    float den[NA];
+    int gp[NA];   // guide code of the output row of each of the thread's ages (its centre pixel)
+    const int abase = SPLIT && hf ? RHO + 1 : 0;   // global age of local age 0
 #pragma unroll
-    for (int a = 0; a < NT; a++) {
+    for (int a = 0; a < NA; a++) {
 #pragma unroll
       for (int q = 0; q < 4; q++) acc[a][q] = make_float2(0.f, 0.f);
       den[a] = 0.f;
-      gp[a] = centre_code(ya - 2 * RHO + a);   // age a at input row 0: output row ya - 2 rho + a
+      gp[a] = centre_code(ya - 2 * RHO + abase + a);   // age at input row 0: output row ya - 2 rho + age
     }
     // clean rows of a whole 8-disparity slab (16-byte aligned): costs staged by cp.async
     // straight into shared memory (skipped pixels zeroed at commit); the nan_map byte and
@@ -265,8 +280,8 @@ __global__ void __launch_bounds__(SM_TX, 2) k_aggregate_small(const SmallArgs A)
       // consumed after the math (its global-load latency hidden behind the row)
       const int gp_next = centre_code(ya - 2 * RHO + i + NT);
       const int st = i & 1;
-      const float* crow = cost + ((size_t)st * CX + tid) * SM_KD;
-      const int* gr = grow + st * CX + tid;
+      const float* crow = cost + ((size_t)st * CX + tc) * SM_KD;
+      const int* gr = grow + st * CX + tc;
       float2 fin[4];
       float fden = 0.f;
 #pragma unroll
@@ -277,15 +292,16 @@ __global__ void __launch_bounds__(SM_TX, 2) k_aggregate_small(const SmallArgs A)
                               make_float2(cb.z, cb.w)};
         const int gq = gr[j];
 #pragma unroll
-        for (int a4 = 0; a4 < (NT + 3) / 4; a4++) {
-          const float4 s4 = *reinterpret_cast<const float4*>(S + j * G::STW + 4 * a4);   // broadcast
+        for (int a4 = 0; a4 < (NA + 3) / 4; a4++) {
+          const float4 s4 =
+              *reinterpret_cast<const float4*>(S + j * G::STW + (SPLIT ? 8 * hf : 0) + 4 * a4);   // broadcast
           const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
           for (int t = 0; t < 4; t++) {
             const int a = 4 * a4 + t;
-            if (a < NT) {
+            if (a < NA) {
               const int idx = min(gq - gp[a] + 255, SM_LUT - 1);
-              const float w = sv[t] * lut[idx * 32 + lane];
+              const float w = sv[t] * lut[idx * REP + (lane & (REP - 1))];
               if (j < NT - 1) {
                 if (CLEAN) den[a] += w;
 #pragma unroll
@@ -304,12 +320,27 @@ __global__ void __launch_bounds__(SM_TX, 2) k_aggregate_small(const SmallArgs A)
           }
         }
       }
+      if (SPLIT) {
+        // the upper half's oldest age (just folded into its fin) becomes the lower half's
+        // newest; the upper half's newest real age starts empty (its dummy age is zero)
+        float2 up[4];
 #pragma unroll
-      for (int q = 0; q < 4; q++) acc[NT - 1][q] = make_float2(0.f, 0.f);
-      den[NT - 1] = 0.f;
+        for (int q = 0; q < 4; q++) {
+          up[q].x = __shfl_xor_sync(0xffffffffu, fin[q].x, 1);
+          up[q].y = __shfl_xor_sync(0xffffffffu, fin[q].y, 1);
+        }
+        const float upd = __shfl_xor_sync(0xffffffffu, fden, 1);
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[NA - 1][q] = hf ? make_float2(0.f, 0.f) : up[q];
+        den[NA - 1] = hf ? 0.f : (CLEAN ? upd : 0.f);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[NT - 1][q] = make_float2(0.f, 0.f);
+        den[NT - 1] = 0.f;
+      }
       // the output row of age 0 completes at input row i
       const int y = ya - 2 * RHO + i;
-      if (y >= ya && x < A.W) {
+      if (hf == 0 && y >= ya && x < A.W) {
         float* o = A.out + (pix0 + (size_t)y * A.W + x) * A.D + k0;
         if (CLEAN) {
           const float inv = rcp_fast(fden);   // fden == 0 exactly for a skipped centre: NaN
@@ -335,9 +366,21 @@ __global__ void __launch_bounds__(SM_TX, 2) k_aggregate_small(const SmallArgs A)
           }
         }
       }
+      if (SPLIT) {
+        const int gup = __shfl_xor_sync(0xffffffffu, gp[0], 1);   // upper half's oldest
 #pragma unroll
-      for (int a = 0; a + 1 < NT; a++) gp[a] = gp[a + 1];
-      gp[NT - 1] = gp_next;
+        for (int a = 0; a + 1 < NA; a++) gp[a] = gp[a + 1];
+        if (hf) {
+          gp[NA - 1] = gp_next;
+          if (NA >= 2) gp[NA - 2] = gp_next;                      // the entering age 2 rho
+        } else {
+          gp[NA - 1] = gup;
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a + 1 < NT; a++) gp[a] = gp[a + 1];
+        gp[NT - 1] = gp_next;
+      }
       if (i + 1 < NR) {
         if (async_rows) commit_async(i + 1, pg, pn);
         else commit_row(i + 1, pv, pg, pn);
@@ -366,19 +409,19 @@ bool aggregate_small_applies(int D, int rho) {
   return !(e && e[0] == '0');
 }
 
-template <int RHO>
+template <int RHO, bool SPLIT>
 static cudaError_t small_launch_t(int B, int H, int W, int D, float gamma_d, float gamma_r, int conc,
                                   const float* vol, const uint8_t* guide, const uint8_t* nan_map, float* out,
                                   cudaStream_t st) {
-  using G = SmallGeom<RHO>;
+  using G = SmallGeom<RHO, SPLIT>;
   SmallArgs A;
   A.B = B; A.H = H; A.W = W; A.D = D;
   A.nslab = (D + SM_KD - 1) / SM_KD;
-  const int nstrip = (W + SM_TX - 1) / SM_TX;
-  // rows per CTA: minimise waves x (R + 2 rho) with 2 CTAs per SM, counting the
+  const int nstrip = (W + G::TXC - 1) / G::TXC;
+  // rows per CTA: minimise waves x (R + 2 rho) with 2 (4 SPLIT) CTAs per SM, counting the
   // aggregations the caller keeps in flight together
   const long long cols = (long long)nstrip * B * A.nslab * (conc > 1 ? conc : 1);
-  const long long slots = 2LL * small_sm_count();
+  const long long slots = (SPLIT ? 4LL : 2LL) * small_sm_count();
   int bestR = H;
   double best = 1e300;
   for (int n = 1; n <= H; n++) {
@@ -395,17 +438,23 @@ static cudaError_t small_launch_t(int B, int H, int W, int D, float gamma_d, flo
   A.vol = vol; A.guide = guide; A.nan_map = nan_map; A.out = out;
   const long long nblk = (long long)nstrip * ((H + bestR - 1) / bestR) * A.nslab * B;
   if (nblk > 0x7fffffffLL) return cudaErrorInvalidValue;
-  cudaError_t e = smem_optin((const void*)k_aggregate_small<RHO>, G::bytes);
+  cudaError_t e = smem_optin((const void*)k_aggregate_small<RHO, SPLIT>, G::bytes);
   if (e != cudaSuccess) return e;
-  k_aggregate_small<RHO><<<(unsigned)nblk, SM_TX, G::bytes, st>>>(A);
+  k_aggregate_small<RHO, SPLIT><<<(unsigned)nblk, SM_TX, G::bytes, st>>>(A);
   return cudaGetLastError();
 }
 
 cudaError_t launch_aggregate_small(int B, int H, int W, int D, int rho, float gamma_d, float gamma_r, int conc,
                                    const float* vol, const uint8_t* guide, const uint8_t* nan_map, float* out,
                                    cudaStream_t st) {
-#define RSR_SM(R) \
-  case R: return small_launch_t<R>(B, H, W, D, gamma_d, gamma_r, conc, vol, guide, nan_map, out, st);
+  // two threads per column (SPLIT) for rho >= 1; RSR_K3_SPLIT=0 keeps one (A/B)
+  const char* e = getenv("RSR_K3_SPLIT");
+  const bool split = !(e && e[0] == '0');
+#define RSR_SM(R)                                                                                         \
+  case R:                                                                                                 \
+    return (split && R >= 1)                                                                              \
+               ? small_launch_t<R, (R >= 1)>(B, H, W, D, gamma_d, gamma_r, conc, vol, guide, nan_map, out, st) \
+               : small_launch_t<R, false>(B, H, W, D, gamma_d, gamma_r, conc, vol, guide, nan_map, out, st);
   switch (rho) {
     RSR_SM(0) RSR_SM(1) RSR_SM(2) RSR_SM(3) RSR_SM(4) RSR_SM(5) RSR_SM(6) RSR_SM(7)
     default:
