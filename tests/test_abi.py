@@ -70,3 +70,36 @@ def test_validation_without_gpu(L):
     assert L.rsr_road_model(s, rp, None, fake, fake, wsr, None) == 2
     assert L.rsr_strerror(2) == b"invalid argument"
     assert L.rsr_version() >= 10000
+
+
+def test_validation_of_round2_calls_without_gpu(L):
+    """rsr_match (f1) and the interpolating-warp calls (f2) validate before any launch."""
+    from paper_1807_07433_b200._lib import RsrAggParams, RsrCostParams, RsrDispParams, RsrShape
+    s = RsrShape(1, 32, 64)
+    fake = ctypes.c_void_p(16)
+    ws = L.rsr_cost_workspace_size(s)
+    cp, ap, dp = RsrCostParams(2, -4, 3), RsrAggParams(3, 2.0, 10.0, 1), RsrDispParams(-4, 3, 1, 1)
+    # D = 17 > 8: the fused kernel serves the small search ranges only
+    assert L.rsr_match(s, RsrCostParams(2, -8, 8), ap, RsrDispParams(-8, 8, 1, 1), fake, fake, fake, fake, fake,
+                       None, None, fake, ws, None) == 2
+    # the disparity range must be the cost range
+    assert L.rsr_match(s, cp, ap, RsrDispParams(-4, 4, 1, 1), fake, fake, fake, fake, fake, None, None, fake, ws,
+                       None) == 2
+    assert L.rsr_match(s, cp, RsrAggParams(8, 2.0, 10.0, 1), dp, fake, fake, fake, fake, fake, None, None, fake, ws,
+                       None) == 2
+    assert L.rsr_match(s, cp, ap, dp, fake, fake, fake, fake, fake, None, None, fake, ws - 1, None) == 2
+    assert L.rsr_match(s, RsrCostParams(20, -4, 3), ap, dp, fake, fake, fake, fake, fake, None, None, fake, ws,
+                       None) == 2
+    assert L.rsr_match(RsrShape(1, 4, 64), cp, ap, dp, fake, fake, fake, fake, fake, None, None, fake, ws,
+                       None) == 3
+    # interpolating warp family
+    assert L.rsr_warp_linear(RsrShape(0, 8, 8), fake, fake, fake, fake, fake, None) == 2
+    assert L.rsr_cost_volume_linear(s, RsrCostParams(0, 0, 3), fake, fake, fake, fake, None, None, None, fake, ws,
+                                    None) == 2
+    assert L.rsr_aggregate_linear(s, 8, RsrAggParams(8, 1.0, 1.0, 1), fake, fake, None, ctypes.c_void_p(32),
+                                  None) == 2   # rho > 7
+    assert L.rsr_disparity_linear(s, RsrDispParams(0, 3, -1, 1), fake, fake, fake, fake, None, None, None) == 2
+    # introspection: row chunk of K3's launch plan
+    assert L.rsr_aggregate_rows(RsrShape(8, 720, 1280), 64, RsrAggParams(6, 4.0, 12.0, 2)) == 240
+    assert L.rsr_aggregate_rows(RsrShape(1, 40, 90), 16, RsrAggParams(8, 4.0, 12.0, 1)) == 0
+    assert L.rsr_aggregate_rows(RsrShape(0, 40, 90), 16, RsrAggParams(2, 4.0, 12.0, 1)) == -1
