@@ -169,6 +169,7 @@ __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g
   const bool bulk = (A.D & 3) == 0;
   const float fillv = clean ? 0.f : qnan();
   const int st = it_c % SG_NSC;
+  RSR_CHECK(st >= 0 && st < SG_NSC && g.CS <= g.KS);
   if (it_c >= SG_NSC) mbar_wait_parity(&empty_c[st], ((it_c / SG_NSC) & 1) ^ 1);
   it_c++;
   const int yy = s.ya - RHO + i;
@@ -183,6 +184,7 @@ __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g
       // the guide tile marks outside and all-NaN pixels: filled, not copied
       const bool skip = !row_in || gt[(i + RHO) * g.CX + col] == gskip<G16>();
       if (!skip && k < s.ks_eff) {
+        RSR_CHECK(col < g.CX && k + 1 < g.KS && s.x0 - RHO + col >= 0 && s.x0 - RHO + col < A.W);
         cp_async8(d, A.vol + (rowpix + (s.x0 - RHO + col)) * A.D + s.k0 + k);
       } else {
         d[0] = fillv;
@@ -222,6 +224,7 @@ __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g
   if (ncols == (uint32_t)g.CX && g.CS == A.D) {
     // whole row segment in the image and one contiguous run: a single bulk copy
     const uint32_t bytes = (uint32_t)g.CX * g.CS * 4u;
+    RSR_CHECK(g.CX * g.CS <= g.CX * g.KS && s.x0 - RHO >= 0 && s.x0 - RHO + g.CX <= A.W);
     if (lane == 0) {
       mbar_arrive_expect_tx(&full_c[st], bytes);
       bulk_g2s(dst, src, bytes, &full_c[st]);
@@ -233,7 +236,10 @@ __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       const int col = lane + 32 * h;
-      if (cp[h]) bulk_g2s(dst + col * g.CS, src + (size_t)col * A.D, bytes_col, &full_c[st]);
+      if (cp[h]) {
+        RSR_CHECK(col * g.CS + s.ks_eff <= g.CX * g.KS && s.x0 - RHO + col >= 0 && s.x0 - RHO + col < A.W);
+        bulk_g2s(dst + col * g.CS, src + (size_t)col * A.D, bytes_col, &full_c[st]);
+      }
     }
   }
 }
@@ -293,6 +299,7 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
       for (int n = 0; n < NAB; n++) {
         const int x = p * 8 + xs, a = n * 4 + as;
         const int ac = min(a, NT - 1);
+        RSR_CHECK((i + ac) < g.GR && (i + RHO) < g.GR && x + 2 * RHO < g.CX);
         int gp = gt[(i + ac) * g.CX + x + RHO];
         float* slot = dsum + ((i + ac) % NT) * 32 + x;
         float d = *slot;
@@ -310,10 +317,14 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
         } else {
           gp = (gp == SG_GSKIP) ? -SG_GSKIP : gp;
 #pragma unroll
-          for (int j = 0; j < NT; j++) w[j] = sreg[n][j] * rlut[trs[x + j] - gp + 255];
+          for (int j = 0; j < NT; j++) {
+            RSR_CHECK(trs[x + j] - gp + 255 >= 0 && trs[x + j] - gp + 255 < SG_RLUT);
+            w[j] = sreg[n][j] * rlut[trs[x + j] - gp + 255];
+          }
         }
         if (a < NT) {
           float* wd = wst + x * g.XS + a;
+          RSR_CHECK(x * g.XS + a + (NT - 1) * 16 < 32 * g.XS && a < 16);
 #pragma unroll
           for (int j = 0; j < NT; j++) {
             wd[j * 16] = w[j];
@@ -457,6 +468,8 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
       mbar_wait_parity(&full_w[stw], (it / SG_NSW) & 1);
       const float* crow = cost_s + (size_t)stc * g.CX * g.KS + xl * g.CS + koff;
       const float* wrow = w_s + (size_t)stw * g.WST + xl * g.XS;
+      RSR_CHECK(xl * g.CS + koff + (NT - 1) * g.CS + (CLEAN ? 4 * g.G : 0) + 4 <= g.CX * g.KS);
+      RSR_CHECK(xl * g.XS + (NT - 1) * 16 + 16 <= 32 * g.XS && xl < 32);
       float2 fin[4];
       if (CLEAN)
         slide_row<RHO, 0>(acc, fin, crow, wrow, g.CS, g.G);
@@ -474,6 +487,7 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
       if (y >= s.ya && x < A.W) {
         const size_t pix = s.pix0 + (size_t)y * A.W + x;
         float* o = A.out + pix * A.D + s.k0 + koff;
+        RSR_CHECK(pix < (size_t)A.B * A.H * A.W);   // k beyond D: never written (predicated below)
         if (CLEAN) {
           // den == 0 exactly when the centre is skipped (all-NaN): 0 * inf = NaN
           const float inv = rcp_fast(den);

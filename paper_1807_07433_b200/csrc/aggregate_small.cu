@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(SM_TX, SPLIT ? 4 : 2) k_aggregate_small(const 
           }
         }
         float4* d = reinterpret_cast<float4*>(cost + ((size_t)st * CX + c) * SM_KD);
+        RSR_CHECK(st < 2 && c < CX);
         d[0] = make_float4(o[0], o[1], o[2], o[3]);
         d[1] = make_float4(o[4], o[5], o[6], o[7]);
         grow[st * CX + c] = skip ? SM_SKIPQ : gv[h];
@@ -301,6 +302,7 @@ __global__ void __launch_bounds__(SM_TX, SPLIT ? 4 : 2) k_aggregate_small(const 
             const int a = 4 * a4 + t;
             if (a < NA) {
               const int idx = min(gq - gp[a] + 255, SM_LUT - 1);
+              RSR_CHECK(idx >= 0 && tc + j < CX);
               const float w = sv[t] * lut[idx * REP + (lane & (REP - 1))];
               if (j < NT - 1) {
                 if (CLEAN) den[a] += w;
@@ -342,6 +344,7 @@ __global__ void __launch_bounds__(SM_TX, SPLIT ? 4 : 2) k_aggregate_small(const 
       const int y = ya - 2 * RHO + i;
       if (hf == 0 && y >= ya && x < A.W) {
         float* o = A.out + (pix0 + (size_t)y * A.W + x) * A.D + k0;
+        RSR_CHECK(y < A.H && x < A.W && k0 + ks_eff <= A.D);
         if (CLEAN) {
           const float inv = rcp_fast(fden);   // fden == 0 exactly for a skipped centre: NaN
           const float r[8] = {fin[0].x * inv, fin[0].y * inv, fin[1].x * inv, fin[1].y * inv,

@@ -8,6 +8,26 @@
 
 #define RSR_DEVINL __device__ __forceinline__
 
+// Bounds checks of our own (compute-sanitizer is closed on this GPU pool): built with
+// -DRSR_CHECKS (tools/checked_run.sh builds librsr_checked.so), every RSR_CHECK that
+// fails prints its file, line and condition and traps the kernel; in the product build
+// it compiles to nothing.
+#ifdef RSR_CHECKS
+#include <cstdio>
+#define RSR_CHECK(cond)                                                                     \
+  do {                                                                                      \
+    if (!(cond)) {                                                                          \
+      printf("rsr check failed: %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+             (int)blockIdx.x, (int)threadIdx.x);                                            \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define RSR_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace rsr {
 
 // Packed fp32x2 FMA (SASS FFMA2) with a scalar operand broadcast to both lanes:

@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(MF_THREADS, 1) k_match_fused(const MatchArgs A
       const int c = e / MF_KD, k = e % MF_KD;
       if (c < VSW) {
         const int wc = c + (D - 1) - k;     // warped column xcl0 - P + c - (d_lo + k), rel. gw0
+        RSR_CHECK(k >= D || (wc >= 0 && wc < GW && c < G::VSW));
         float v = vs[u];
         if (k < D) {
           if (i == 0) {
@@ -298,6 +299,7 @@ __global__ void __launch_bounds__(MF_THREADS, 1) k_match_fused(const MatchArgs A
       const int c = e / MF_KD, k = e % MF_KD;
       float cv = qnan();
       if (k < D) {
+        RSR_CHECK(c + 2 * P < VSW && c + (D - 1) - k < CW + D - 1);
         float hs = VS[c * MF_KD + k];
         for (int dx = 1; dx <= 2 * P; dx++) hs += VS[(c + dx) * MF_KD + k];
         const float sF = st[c], iF = st[CW + c];
@@ -325,6 +327,7 @@ __global__ void __launch_bounds__(MF_THREADS, 1) k_match_fused(const MatchArgs A
       int nanm = 0;
 #pragma unroll
       for (int k = 0; k < MF_KD; k++) {
+        RSR_CHECK(k >= D || (tar ? cc + k : cc + D - 1) < CW);
         v[k] = k < D ? CL[(tar ? cc + k : cc + D - 1) * MF_KD + k] : qnan();
         if (!(v[k] == v[k])) nanm |= 1 << k;
       }
@@ -342,6 +345,7 @@ __global__ void __launch_bounds__(MF_THREADS, 1) k_match_fused(const MatchArgs A
     if (i + 1 < NR) fetch_rows(yin + 1 + P, yin + 1);
     // ---- A: sliding aggregation of the thread's column ----
     const int gbase = gslot * (RC + TC) + (is_tar ? RC + col : col);
+    RSR_CHECK(col + NT - 1 < (is_tar ? TC : RC) && gslot < G::NRG);
     const float* crow = (is_tar ? T0 : R0) + col * MF_KD;
     {
       // window mask of this input row: OR of the NaN bits of the 2 rho + 1 taps
@@ -459,6 +463,7 @@ __global__ void __launch_bounds__(MF_THREADS, 1) k_match_fused(const MatchArgs A
       if (kbest >= 0) {
         const int up = xg - (kbest + d_lo);
         if (up >= 0 && up < W) {
+          RSR_CHECK(up - xt0 >= 0 && up - xt0 < MF_TXT);
           const int kr = krow[up - xt0];
           if (kr >= 0 && abs(kbest - kr) <= A.lrc_tol) {
             float r = (float)(kbest + d_lo);

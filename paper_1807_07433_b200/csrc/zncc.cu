@@ -315,6 +315,7 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
           Fs[slot * gm.FC + e] = u2f(pi_[u]);
         } else if (e < NIMG) {
           const int o = orient_g(e - gm.FC);
+          RSR_CHECK(o >= 0 && o < gm.GROW && slot < gm.NRING);
           const float v = u2f(pi_[u]);
           Gs[slot * gm.GROW + o] = v;
           if (o > 0) Gs1[slot * gm.GROW + o - 1] = v;
@@ -371,6 +372,7 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
   auto accumulate_row = [&](int t, bool subtract) {
     const int slot = t % (2 * P + 3);
     float f[NF4 * 4], ge[NG4 * 4], go[NG4 * 4];
+    RSR_CHECK(slot < gm.NRING && f_start + NF4 * 4 <= gm.FC && grun >= 0 && grun + NG4 * 4 <= gm.GROW);
     const float4* fr = reinterpret_cast<const float4*>(Fs + slot * gm.FC + f_start);
     const float4* gr = reinterpret_cast<const float4*>(Gs + slot * gm.GROW + grun);
     const float4* gr1 = reinterpret_cast<const float4*>(Gs1 + slot * gm.GROW + grun);
@@ -419,6 +421,7 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
         const float4 c = *reinterpret_cast<const float4*>(st + ZTX + ZX * cg);
         sF[0] = a.x; sF[1] = a.y; sF[2] = a.z; sF[3] = a.w;
         iF[0] = c.x; iF[1] = c.y; iF[2] = c.z; iF[3] = c.w;
+        RSR_CHECK(srun >= 0 && srun + NS4 * 4 <= gm.SROW2 && ZX * cg + ZX <= ZTX);
         const float* sg = st + 2 * ZTX + srun;
 #pragma unroll
         for (int i = 0; i < NS4; i++) {
@@ -480,6 +483,7 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
         }
         if (u < W) {
           float* dst = vrow + (size_t)u * Dst + (r0 - d_lo);
+          RSR_CHECK(yy < H && koff + (r0 - d_lo) + nq <= Dst);
           if ((Dst & 3) == 0 && (koff & 3) == 0 && nq >= ZR) {
             reinterpret_cast<float4*>(dst)[0] = make_float4(out[0].x, out[0].y, out[1].x, out[1].y);
             reinterpret_cast<float4*>(dst)[1] = make_float4(out[2].x, out[2].y, out[3].x, out[3].y);
