@@ -305,12 +305,10 @@ __global__ void __launch_bounds__(MF_THREADS, 1) k_match_fused(const MatchArgs A
         const float sF = st[c], iF = st[CW + c];
         const int wc = c + (D - 1) - k;
         const float sG = st[2 * CW + wc], iG = st[2 * CW + (CW + D - 1) + wc];
-        // n S_lw - S_l S_w with error-free products (zncc.cu), then (num * inv_L) * inv_W
-        const float a = nf * hs;
-        const float ae = fmaf(nf, hs, -a);
+        // n S_lw - S_l S_w as in zncc.cu (error-free S_l S_w, one FMA), then (num * inv_L) * inv_W
         const float bb = sF * sG;
         const float be = fmaf(sF, sG, -bb);
-        const float num = (a - bb) + (ae - be);
+        const float num = fmaf(nf, hs, -bb) - be;
         cv = clamp_unit_nan((num * iF) * iG);
       }
       CL[e] = cv;

@@ -466,12 +466,13 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
           const float2 ig = (o & 1) ? make_float2(iGo[o - 1], iGo[o]) : make_float2(iGe[o], iGe[o + 1]);
           const float2 sf = make_float2(sF[i], sF[i]), inf = make_float2(iF[i], iF[i]);
           const float2 nn = make_float2(nf, nf);
-          // n S_lw - S_l S_w with error-free products (cancellation-safe)
-          const float2 a = f2mul(nn, hs[qp]);
-          const float2 ae = f2fma(nn, hs[qp], make_float2(-a.x, -a.y));
+          // n S_lw - S_l S_w: the product S_l S_w split error-free (bb + be), then one
+          // FMA forms n S_lw - bb exactly rounded; exact whenever |num| < 2^24 - 8
+          // (cancellation), 1e-7 relative otherwise
           const float2 bb = f2mul(sf, sg);
-          const float2 be = f2fma(sf, sg, make_float2(-bb.x, -bb.y));
-          const float2 num = f2add(f2sub(a, bb), f2sub(ae, be));
+          const float2 nbb = make_float2(-bb.x, -bb.y);
+          const float2 be = f2fma(sf, sg, nbb);
+          const float2 num = f2sub(f2fma(nn, hs[qp], nbb), be);
           // (num * inv_L) * inv_W, in this order for both volumes (bitwise dual identity)
           const float2 c = TAR ? f2mul(f2mul(num, ig), inf) : f2mul(f2mul(num, inf), ig);
           out[qp] = make_float2(clamp_unit_nan(c.x), clamp_unit_nan(c.y));
