@@ -20,3 +20,4 @@ CMD1="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD1 > gpurun_out/${TAG}_plain1.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-k_aggregate} -s ${NCU_SKIP:-2} -c 1 \
   -o gpurun_out/${TAG}_k3 -f $CMD1 > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu2 rc=$?"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/${TAG}_smoke.log
