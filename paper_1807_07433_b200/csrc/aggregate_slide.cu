@@ -53,17 +53,26 @@ constexpr short SG_GSKIP = 600;     // integer guide tile: skipped pixel (outsid
 // table), 0xFFFF for 8.8 fixed-point guides (NEXT f2: values <= 65280)
 template <bool G16>
 RSR_DEVINL int gskip() { return G16 ? 0xFFFF : SG_GSKIP; }
-constexpr int SG_RLUT = 2 * 600 + 255 + 1;   // range table, zero beyond |dg| = 255
+// range table exp2(kr dg^2) at index dg + 255 (dg in [-255, 255]), entry 511 = 0: the
+// index is clamped to 511, which the skip encodings (tap 600, centre -600) always reach.
+// RC copies interleaved (entry i of copy c at i * RC + c; lane l reads copy l % RC):
+// with RC = 16 two lanes of a warp meet in a bank only with probability 1/2, instead
+// of the ~3.5-way conflicts of random indices into one table.  16 copies in the
+// one-CTA-per-SM kernels (uint8 guide), one in the two-CTA and fixed-point variants.
+constexpr int SG_RLUT = 512;
+constexpr int SG_RCMAX = 16;
+__host__ __device__ constexpr int slide_rc(int minb, bool g16) { return (minb == 1 && !g16) ? SG_RCMAX : 1; }
 
 struct SlideGeom {
-  int G, KS, CS, nslab, CX, XS, WST, GR;
+  int G, KS, CS, nslab, CX, XS, WST, GR, RC;
   size_t off_cost, off_w, off_dpart, off_guide, off_rlut, off_bar, bytes;
 };
 
 // KS = disparities per slab (multiple of 8, <= 64), G = consumer lanes per column
 // rows = output rows the guide tile must hold (SG_SEGMAX for the one-CTA-per-SM
 // kernels; the launch's R for the two-CTA variants, which need the space)
-__host__ __device__ inline SlideGeom slide_geom(int D, int rho, int rows = SG_SEGMAX, bool compact = false) {
+__host__ __device__ inline SlideGeom slide_geom(int D, int rho, int rows = SG_SEGMAX, bool compact = false,
+                                                int rc = 1) {
   SlideGeom g;
   const int NT = 2 * rho + 1;
   g.nslab = (D + 63) / 64;
@@ -80,13 +89,14 @@ __host__ __device__ inline SlideGeom slide_geom(int D, int rho, int rows = SG_SE
   g.XS = 16 * NT + 4;                 // == 20 (mod 32): 4 / 8 columns hit distinct banks
   g.WST = 32 * g.XS + 32;             // weights [x][tap][age16] + completing rows' weight sums
   g.GR = rows + 4 * rho;
+  g.RC = rc;
   size_t o = 0;
   g.off_cost = o;  o += sizeof(float) * (size_t)SG_NSC * g.CX * g.KS;
   g.off_w = o;     o += sizeof(float) * (size_t)SG_NSW * g.WST;
   g.off_dpart = o; o += sizeof(float) * (size_t)NT * 32;
   g.off_guide = o; o += sizeof(short) * (size_t)g.GR * g.CX;
   o = (o + 15) & ~size_t(15);
-  g.off_rlut = o;  o += sizeof(float) * (size_t)SG_RLUT;
+  g.off_rlut = o;  o += sizeof(float) * (size_t)SG_RLUT * g.RC;
   o = (o + 15) & ~size_t(15);
   g.off_bar = o;   o += 8 * (2 * SG_NSC + 2 * SG_NSW);
   g.bytes = o;
@@ -254,7 +264,7 @@ __device__ __forceinline__ void stage_row(const SlideArgs& A, const SlideGeom& g
 // FFMA2 accumulates its per-disparity denominators: both paths give bitwise
 // identical results wherever both apply, whatever the segmentation (batch-size
 // independence).  Warp 0 also stages the cost rows.
-template <int RHO, bool G16>
+template <int RHO, bool G16, int RC>
 __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideGeom& g, const Seg& s,
                                                 bool clean, int npass, const unsigned short* gt, float* w_s,
                                                 float* dsum, float* cost_s, uint64_t* full_w,
@@ -295,6 +305,11 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
       // for the whole kernel (sreg), range factor from a shared table indexed by the
       // integer guide difference (skipped pixels index the zero tail of the table).
       const unsigned short* trs = gt + (i + RHO) * g.CX;   // tap row r
+      // the tap row's guide values of this lane's column, loaded once for its NAB items
+      // (reloaded per item otherwise: the item's stores may alias the tile)
+      int gq[NT];
+#pragma unroll
+      for (int j = 0; j < NT; j++) gq[j] = trs[p * 8 + xs + j];
 #pragma unroll
       for (int n = 0; n < NAB; n++) {
         const int x = p * 8 + xs, a = n * 4 + as;
@@ -310,16 +325,16 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
           const bool pskip = gp == gskip<G16>();
 #pragma unroll
           for (int j = 0; j < NT; j++) {
-            const int gq = trs[x + j];
-            const float dg = (float)(gq - gp);
-            w[j] = (pskip || gq == gskip<G16>()) ? 0.f : sreg[n][j] * ex2_ftz(A.kr * (dg * dg));
+            const float dg = (float)(gq[j] - gp);
+            w[j] = (pskip || gq[j] == gskip<G16>()) ? 0.f : sreg[n][j] * ex2_ftz(A.kr * (dg * dg));
           }
         } else {
           gp = (gp == SG_GSKIP) ? -SG_GSKIP : gp;
 #pragma unroll
           for (int j = 0; j < NT; j++) {
-            RSR_CHECK(trs[x + j] - gp + 255 >= 0 && trs[x + j] - gp + 255 < SG_RLUT);
-            w[j] = sreg[n][j] * rlut[trs[x + j] - gp + 255];
+            const int ix = min(gq[j] - gp + 255, SG_RLUT - 1);
+            RSR_CHECK(ix >= 0 && ix < SG_RLUT);
+            w[j] = sreg[n][j] * rlut[ix * RC];   // rlut: this lane's copy
           }
         }
         if (a < NT) {
@@ -536,15 +551,16 @@ template <int RHO, int MINB, bool COMPACT, bool G16>
 __global__ void __launch_bounds__(MINB == 1 ? 384 : (RHO <= 5 ? 256 : 192), MINB)
     k_aggregate_slide(const SlideArgs A) {
   extern __shared__ __align__(128) unsigned char sl_smem[];
-  const SlideGeom g = slide_geom(A.D, RHO, MINB == 1 ? SG_SEGMAX : A.R, COMPACT);
+  constexpr int RC = slide_rc(MINB, G16);
+  const SlideGeom g = slide_geom(A.D, RHO, A.R, COMPACT, RC);
   float* cost_s = reinterpret_cast<float*>(sl_smem + g.off_cost);
   float* w_s = reinterpret_cast<float*>(sl_smem + g.off_w);
   float* dpart = reinterpret_cast<float*>(sl_smem + g.off_dpart);
   unsigned short* gt = reinterpret_cast<unsigned short*>(sl_smem + g.off_guide);
   float* rlut = reinterpret_cast<float*>(sl_smem + g.off_rlut);
-  // range factor exp2(kr dg^2) at index dg + 255; zero for the skip encodings
-  for (int t = threadIdx.x; t < SG_RLUT; t += blockDim.x) {
-    const int dg = t - 255;
+  // range factor exp2(kr dg^2) at index dg + 255 (RC interleaved copies); entry 511 = 0
+  for (int t = threadIdx.x; t < SG_RLUT * RC; t += blockDim.x) {
+    const int dg = t / RC - 255;
     rlut[t] = (dg >= -255 && dg <= 255) ? ex2_ftz((float)(dg * dg) * A.kr) : 0.f;
   }
   uint64_t* full_c = reinterpret_cast<uint64_t*>(sl_smem + g.off_bar);
@@ -613,8 +629,8 @@ __global__ void __launch_bounds__(MINB == 1 ? 384 : (RHO <= 5 ? 256 : 192), MINB
     const int hcmask = (__syncthreads_or(dirty & 1) ? 0 : 1) | (__syncthreads_or(dirty & 2) ? 0 : 2);
     const int npass = clean ? 1 : 2;
     if (warp >= n_cons) {
-      produce_weights<RHO, G16>(A, g, s, clean, npass, gt, w_s, dpart, cost_s, full_w, empty_w, full_c, empty_c,
-                           it, it_c, warp - n_cons, lane, rlut);
+      produce_weights<RHO, G16, RC>(A, g, s, clean, npass, gt, w_s, dpart, cost_s, full_w, empty_w, full_c,
+                                    empty_c, it, it_c, warp - n_cons, lane, rlut + (lane & (RC - 1)));
     } else {
       const int t = tid;   // consumer thread: column t / G, lane-in-group t % G
       if (clean)
@@ -651,7 +667,10 @@ static SlidePlan slide_plan(int B, int H, int W, int D, int rho, int conc, int n
   const long long cols = (long long)nstrips * B * g1.nslab;
   const bool small = g1.G <= (rho <= 5 ? 4 : 2);
   const int minb = small ? 2 : 1;
-  auto fits = [&](int R) { return minb == 1 || slide_geom(D, rho, R).bytes <= 113 * 1024; };
+  // the guide tile holds the launch's R rows (+ halo) next to the range-table copies
+  auto fits = [&](int R) {
+    return slide_geom(D, rho, R, false, slide_rc(minb, false)).bytes <= (minb == 1 ? 227 : 113) * 1024;
+  };
   const long long inflight = conc > 1 ? conc : 1;
   int bestR = 0;
   double best = 1e300;
@@ -674,7 +693,7 @@ static SlidePlan slide_plan(int B, int H, int W, int D, int rho, int conc, int n
   // compact cost rows (one bulk copy per row) where D < KS and rows stay aligned; the
   // compact kernels spill a little more, so D == KS keeps the padded layout
   p.compact = small && g1.nslab == 1 && (D & 3) == 0 && D < g1.KS;
-  p.bytes = minb == 1 ? g1.bytes : slide_geom(D, rho, bestR).bytes;
+  p.bytes = slide_geom(D, rho, bestR, p.compact, slide_rc(minb, false)).bytes;
   return p;
 }
 
@@ -707,9 +726,11 @@ static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, flo
   auto kern = plan.minb == 1 ? k_aggregate_slide<RHO, 1, false, G16>
                              : (plan.compact ? k_aggregate_slide<RHO, 2, true, G16>
                                              : k_aggregate_slide<RHO, 2, false, G16>);
-  cudaError_t e = smem_optin((const void*)kern, plan.bytes);
+  // the fixed-point guide's range factor is computed (MUFU): one (unused) table copy
+  const size_t bytes = slide_geom(D, RHO, plan.R, plan.compact, slide_rc(plan.minb, G16)).bytes;
+  cudaError_t e = smem_optin((const void*)kern, bytes);
   if (e != cudaSuccess) return e;
-  kern<<<(unsigned)nblk, 32 * (g1.G + SG_NPROD), plan.bytes, st>>>(A);
+  kern<<<(unsigned)nblk, 32 * (g1.G + SG_NPROD), bytes, st>>>(A);
   return cudaGetLastError();
 }
 

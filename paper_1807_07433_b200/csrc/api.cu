@@ -42,8 +42,9 @@ int rsr_warp(rsr_shape s, const double* alpha_beta, const uint8_t* target, uint8
 
 size_t rsr_cost_workspace_size(rsr_shape s) {
   if (!shape_ok(s)) return 0;
-  // S_L (int32), inv_L (f32), S_W (int32), inv_W (f32), each [B][H][W]
-  return 4 * align16(sizeof(int32_t) * npix(s));
+  // S_L, inv_L, S_W, inv_W, each [B][H][W] (S int32, or fp32 for rsr_cost_volume), and
+  // for rsr_cost_volume the fp32 copies of both images the NCC kernel streams
+  return 6 * align16(sizeof(int32_t) * npix(s));
 }
 
 int rsr_cost_volume(rsr_shape s, rsr_cost_params p, const uint8_t* ref, const uint8_t* warped,
@@ -59,33 +60,35 @@ int rsr_cost_volume(rsr_shape s, rsr_cost_params p, const uint8_t* ref, const ui
   if ((size_t)(s.height + 15) / 16 > 65535 || s.batch > 65535) return RSR_E_ARG;
   const size_t chunk = align16(sizeof(int32_t) * npix(s));
   char* ws = static_cast<char*>(workspace);
-  int32_t* SL = reinterpret_cast<int32_t*>(ws);
+  float* SL = reinterpret_cast<float*>(ws);
   float* iL = reinterpret_cast<float*>(ws + chunk);
-  int32_t* SW = reinterpret_cast<int32_t*>(ws + 2 * chunk);
+  float* SW = reinterpret_cast<float*>(ws + 2 * chunk);
   float* iW = reinterpret_cast<float*>(ws + 3 * chunk);
+  float* Lf = reinterpret_cast<float*>(ws + 4 * chunk);
+  float* Wf = reinterpret_cast<float*>(ws + 5 * chunk);
   cudaStream_t st = as_stream(stream);
   // both images' block statistics in one grid (two grids past 65535 / 2 frames)
   cudaError_t e;
   if (2LL * s.batch <= 65535) {
-    e = rsr::launch_block_stats(s.batch, s.height, s.width, p.rho_block, ref, nullptr, SL, iL, warped, valid,
-                                SW, iW, st);
+    e = rsr::launch_block_stats_f(s.batch, s.height, s.width, p.rho_block, ref, nullptr, SL, iL, Lf, warped,
+                                  valid, SW, iW, Wf, st);
   } else {
-    e = rsr::launch_block_stats(s.batch, s.height, s.width, p.rho_block, ref, nullptr, SL, iL, nullptr,
-                                nullptr, nullptr, nullptr, st);
+    e = rsr::launch_block_stats_f(s.batch, s.height, s.width, p.rho_block, ref, nullptr, SL, iL, Lf, nullptr,
+                                  nullptr, nullptr, nullptr, nullptr, st);
     if (e == cudaSuccess)
-      e = rsr::launch_block_stats(s.batch, s.height, s.width, p.rho_block, warped, valid, SW, iW, nullptr,
-                                  nullptr, nullptr, nullptr, st);
+      e = rsr::launch_block_stats_f(s.batch, s.height, s.width, p.rho_block, warped, valid, SW, iW, Wf,
+                                    nullptr, nullptr, nullptr, nullptr, nullptr, st);
   }
   if (e == cudaSuccess && vol_tar && 2LL * s.batch <= 65535)   // both volumes, one grid
-    e = rsr::launch_zncc_pair(s.batch, s.height, s.width, p.rho_block, p.d_lo, (int)D, ref, warped, SL, iL,
+    e = rsr::launch_zncc_pair(s.batch, s.height, s.width, p.rho_block, p.d_lo, (int)D, Lf, Wf, SL, iL,
                               SW, iW, vol_ref, vol_tar, st);
   else {
     if (e == cudaSuccess)
-      e = rsr::launch_zncc(false, s.batch, s.height, s.width, p.rho_block, p.d_lo, (int)D, ref,
-                           warped, SL, iL, SW, iW, vol_ref, st);
+      e = rsr::launch_zncc(false, s.batch, s.height, s.width, p.rho_block, p.d_lo, (int)D, Lf,
+                           Wf, SL, iL, SW, iW, vol_ref, st);
     if (e == cudaSuccess && vol_tar)
-      e = rsr::launch_zncc(true, s.batch, s.height, s.width, p.rho_block, p.d_lo, (int)D, ref,
-                           warped, SL, iL, SW, iW, vol_tar, st);
+      e = rsr::launch_zncc(true, s.batch, s.height, s.width, p.rho_block, p.d_lo, (int)D, Lf,
+                           Wf, SL, iL, SW, iW, vol_tar, st);
   }
   if (e == cudaSuccess)
     e = rsr::launch_nan_maps(s.batch, s.height, s.width, p.d_lo, (int)D, iL, iW, nan_ref,

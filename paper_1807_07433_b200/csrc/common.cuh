@@ -127,8 +127,16 @@ RSR_DEVINL void cp_async8(void* smem_dst, const void* gsrc) {
 RSR_DEVINL void cp_async16(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
 }
+// 4-byte asynchronous global -> shared copy (cp.async.ca, LDGSTS), group-tracked.  No
+// memory clobber: callers order the copy against shared-memory reads of its slot with
+// a CTA barrier (and cp_async_wait_* before reading), both of which are compiler fences.
+RSR_DEVINL void cp_async4(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem_dst)), "l"(gsrc));
+}
 RSR_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 RSR_DEVINL void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// every committed group but the most recent one has landed (this thread's copies)
+RSR_DEVINL void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 // arrive on bar once every cp.async this thread issued so far has landed (counts as
 // one of the barrier's expected arrivals)

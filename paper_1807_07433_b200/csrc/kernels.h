@@ -20,15 +20,22 @@ cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* im
                                int32_t* S0, float* inv0, const uint8_t* img1, const uint8_t* mask1, int32_t* S1,
                                float* inv1, cudaStream_t st);
 
+// The same statistics for the streaming NCC kernel: S as fp32 (exact) and each image
+// also as an fp32 plane (F0 = img0, F1 = img1); img1 may be null.
+cudaError_t launch_block_stats_f(int B, int H, int W, int rho_b, const uint8_t* img0, const uint8_t* mask0,
+                                 float* S0, float* inv0, float* F0, const uint8_t* img1, const uint8_t* mask1,
+                                 float* S1, float* inv1, float* F1, cudaStream_t st);
+
 // NCC volume in [B][H][W][D] layout. tar=false: vol[v][u][k] = c(u, v, r);
-// tar=true: vol[v][u'][k] = c(u'+r, v, r).
+// tar=true: vol[v][u'][k] = c(u'+r, v, r).  Inputs: the fp32 planes of
+// launch_block_stats_f (images Lf = ref, Wf = warped; sums; norms).
 // both volumes in one launch (grid of 2B frames)
-cudaError_t launch_zncc_pair(int B, int H, int W, int rho_b, int d_lo, int D, const uint8_t* ref,
-                             const uint8_t* warped, const int32_t* SL, const float* invL, const int32_t* SW,
+cudaError_t launch_zncc_pair(int B, int H, int W, int rho_b, int d_lo, int D, const float* ref,
+                             const float* warped, const float* SL, const float* invL, const float* SW,
                              const float* invW, float* vol_ref, float* vol_tar, cudaStream_t st);
 cudaError_t launch_zncc(bool tar, int B, int H, int W, int rho_b, int d_lo, int D,
-                        const uint8_t* ref, const uint8_t* warped, const int32_t* SL,
-                        const float* invL, const int32_t* SW, const float* invW, float* vol,
+                        const float* ref, const float* warped, const float* SL,
+                        const float* invL, const float* SW, const float* invW, float* vol,
                         cudaStream_t st);
 
 // block statistics with an 8.8 fixed-point second image (NEXT f2)

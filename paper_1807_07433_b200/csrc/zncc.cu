@@ -39,19 +39,25 @@ constexpr int ST_TX = 64, ST_TY = 32;   // 32 rows: 47 KB of shared memory at p 
 // img0 is uint8 (the reference image); img1 is uint8 or, for the interpolating
 // warp (NEXT f2), the 8.8 fixed-point warped image (uint16): sums of squares then
 // need int64 (225 * 65280^2 > 2^31).
-template <int p, typename T1>
+// FOUT (the streaming NCC kernel's inputs): S is stored as fp32 (exact: < 2^24) and
+// each image is also written as an fp32 plane (img0 -> F0, img1 -> F1), so that
+// k_zncc can stage its rows with 4-byte cp.async copies and no conversion.
+template <int p, typename T1, bool FOUT = false>
 __global__ void __launch_bounds__(256) k_block_stats(int B, int H, int W,
                                                      const uint8_t* __restrict__ img0,
                                                      const uint8_t* __restrict__ mask0,
                                                      int32_t* __restrict__ S0, float* __restrict__ inv0,
                                                      const T1* __restrict__ img1,
                                                      const uint8_t* __restrict__ mask1,
-                                                     int32_t* __restrict__ S1, float* __restrict__ inv1) {
+                                                     int32_t* __restrict__ S1, float* __restrict__ inv1,
+                                                     float* __restrict__ F0 = nullptr,
+                                                     float* __restrict__ F1 = nullptr) {
   using SST = typename std::conditional<sizeof(T1) == 1, int, long long>::type;
   const bool second = (int)blockIdx.z >= B;
   const uint8_t* __restrict__ mask = second ? mask1 : mask0;
   int32_t* __restrict__ Sout = second ? S1 : S0;
   float* __restrict__ inv = second ? inv1 : inv0;
+  float* __restrict__ Fout = second ? F1 : F0;
   extern __shared__ __align__(16) unsigned char st_raw[];
   const int TC = ST_TX + 2 * p, TR = ST_TY + 2 * p;
   SST* cSS = reinterpret_cast<SST*>(st_raw);         // [ST_TY][TC] vertical sums of squares
@@ -113,15 +119,20 @@ __global__ void __launch_bounds__(256) k_block_stats(int B, int H, int W,
     const long long var = (long long)n * ss - (long long)s * s;
     const bool ok = inside && m == n && var != 0;
     const size_t g = base + (size_t)yy * W + xx;
-    Sout[g] = s;
+    if (FOUT) {
+      reinterpret_cast<float*>(Sout)[g] = (float)s;
+      Fout[g] = (float)pix[(y + p) * TC + x + p];
+    } else {
+      Sout[g] = s;
+    }
     inv[g] = ok ? rsqrtf((float)var) : qnan();
   }
 }
 
-template <typename T1>
+template <typename T1, bool FOUT = false>
 static cudaError_t block_stats_t(int B, int H, int W, int rho_b, const uint8_t* img0, const uint8_t* mask0,
                                  int32_t* S0, float* inv0, const T1* img1, const uint8_t* mask1, int32_t* S1,
-                                 float* inv1, cudaStream_t st) {
+                                 float* inv1, cudaStream_t st, float* F0 = nullptr, float* F1 = nullptr) {
   using SST = typename std::conditional<sizeof(T1) == 1, int, long long>::type;
   const int p = rho_b;
   const int TC = ST_TX + 2 * p, TR = ST_TY + 2 * p;
@@ -132,9 +143,10 @@ static cudaError_t block_stats_t(int B, int H, int W, int rho_b, const uint8_t* 
   switch (p) {
 #define RSR_BS(PP)                                                                              \
   case PP: {                                                                                    \
-    const cudaError_t e = smem_optin((const void*)k_block_stats<PP, T1>, smem);                \
+    const cudaError_t e = smem_optin((const void*)k_block_stats<PP, T1, FOUT>, smem);          \
     if (e != cudaSuccess) return e;                                                             \
-    k_block_stats<PP, T1><<<grid, 256, smem, st>>>(B, H, W, img0, mask0, S0, inv0, img1, mask1, S1, inv1); \
+    k_block_stats<PP, T1, FOUT><<<grid, 256, smem, st>>>(B, H, W, img0, mask0, S0, inv0, img1, mask1, S1, \
+                                                         inv1, F0, F1);                         \
     break;                                                                                      \
   }
     RSR_BS(1) RSR_BS(2) RSR_BS(3) RSR_BS(4) RSR_BS(5) RSR_BS(6) RSR_BS(7)
@@ -150,6 +162,13 @@ cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* im
   return block_stats_t<uint8_t>(B, H, W, rho_b, img0, mask0, S0, inv0, img1, mask1, S1, inv1, st);
 }
 
+cudaError_t launch_block_stats_f(int B, int H, int W, int rho_b, const uint8_t* img0, const uint8_t* mask0,
+                                 float* S0, float* inv0, float* F0, const uint8_t* img1, const uint8_t* mask1,
+                                 float* S1, float* inv1, float* F1, cudaStream_t st) {
+  return block_stats_t<uint8_t, true>(B, H, W, rho_b, img0, mask0, reinterpret_cast<int32_t*>(S0), inv0, img1,
+                                      mask1, reinterpret_cast<int32_t*>(S1), inv1, st, F0, F1);
+}
+
 cudaError_t launch_block_stats16(int B, int H, int W, int rho_b, const uint8_t* img0, int32_t* S0, float* inv0,
                                  const uint16_t* img1, const uint8_t* mask1, int32_t* S1, float* inv1,
                                  cudaStream_t st) {
@@ -160,9 +179,10 @@ cudaError_t launch_block_stats16(int B, int H, int W, int rho_b, const uint8_t* 
 // NCC volume kernel (streaming).  A CTA owns ZTX = 64 columns x all D (up to
 // 128) disparities and slides down ZBY rows.  Image rows and the block
 // statistics of the current output row stream through a small shared-memory
-// ring: every iteration first issues the global loads of the rows needed one
-// iteration later (kept in registers), computes the current row, then commits
-// the prefetched rows to the ring, so the load latency overlaps the math.
+// ring: every iteration first issues 4-byte cp.async copies (fp32 planes from
+// k_block_stats<FOUT>) of the rows needed two iterations later, straight into
+// their oriented ring slots, then computes the current row, so the copy latency
+// overlaps the math and no thread spends instructions on conversion or commits.
 // ---------------------------------------------------------------------------
 constexpr int ZX = 4;     // columns per thread
 constexpr int ZR = 8;     // disparities per thread (4 packed pairs)
@@ -190,9 +210,10 @@ struct ZnccGeom {
 __host__ __device__ inline ZnccGeom zncc_geom(int p, int D, int ZTX = rsr::ZTX) {
   ZnccGeom g;
   const int NJ = ZX + 2 * p;
-  // image rows y-1 .. y+2p being read, plus the one committed for the next row into
-  // the slot of y-2 (last read one iteration earlier): one barrier per row
-  g.NRING = 2 * p + 3;
+  // image rows y-1 .. y+2p being read, row y+2p+1 in flight (issued one iteration
+  // earlier) and row y+2p+2 issued now into the slot of y-2 (last read one iteration
+  // earlier): one barrier per row, copies issued two rows ahead
+  g.NRING = 2 * p + 4;
   g.FC = ((ZTX + 2 * p + 3) / 4) * 4 + 4;
   g.gpad = (4 - (D & 3)) & 3;
   g.GC = ((ZTX + 2 * p + D - 1 + g.gpad + 3) / 4) * 4 + 8;
@@ -207,9 +228,9 @@ __host__ __device__ inline ZnccGeom zncc_geom(int p, int D, int ZTX = rsr::ZTX) 
 
 __host__ __device__ inline size_t zncc_smem(int p, int D, int ZTX = rsr::ZTX, bool shear = false) {
   const ZnccGeom g = zncc_geom(p, D, ZTX);
-  // ring: F rows, oriented G rows x2; statistics double buffer: sF, iF, sG x2, iG x2;
+  // ring: F rows, oriented G rows x2; statistics triple buffer: sF, iF, sG x2, iG x2;
   // SHEAR: the reference tile of the row [ZTX][ZT_STR]
-  return sizeof(float) * ((size_t)g.NRING * (g.FC + 2 * g.GROW) + 2 * (2 * ZTX + 4 * (size_t)g.SROW2) +
+  return sizeof(float) * ((size_t)g.NRING * (g.FC + 2 * g.GROW) + 3 * (2 * ZTX + 4 * (size_t)g.SROW2) +
                           (shear ? (size_t)ZTX * 68 : 0));
 }
 
@@ -224,11 +245,11 @@ constexpr int ZT_STR = 68;   // shared tile row stride (floats): conflict-free d
 
 template <int P, bool TAR, int ZTX = rsr::ZTX, bool SHEAR = false>
 __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, int Dst, int koff,
-                                              const uint8_t* __restrict__ ref,
-                                              const uint8_t* __restrict__ warped,
-                                              const int32_t* __restrict__ SLg,
+                                              const float* __restrict__ ref,
+                                              const float* __restrict__ warped,
+                                              const float* __restrict__ SLg,
                                               const float* __restrict__ invLg,
-                                              const int32_t* __restrict__ SWg,
+                                              const float* __restrict__ SWg,
                                               const float* __restrict__ invWg,
                                               float* __restrict__ vol,
                                               float* __restrict__ vol_tar = nullptr) {
@@ -244,19 +265,20 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
   float* Fs = zsm;                                   // [NRING][FC]    F image rows
   float* Gs = Fs + gm.NRING * gm.FC;                 // [NRING][GROW]  oriented G image rows
   float* Gs1 = Gs + gm.NRING * gm.GROW;              // [NRING][GROW]  shifted by one entry
-  float* St = Gs1 + gm.NRING * gm.GROW;              // [2][sF ZTX | iF ZTX | sG | sG1 | iG | iG1]
+  float* St = Gs1 + gm.NRING * gm.GROW;              // [3][sF ZTX | iF ZTX | sG | sG1 | iG | iG1]
   const int SROW = 2 * ZTX + 4 * gm.SROW2;
-  float* Tt = St + 2 * SROW;                         // SHEAR: [ZTX][ZT_STR] reference costs of the row
+  float* Tt = St + 3 * SROW;                         // SHEAR: [ZTX][ZT_STR] reference costs of the row
+  constexpr int NRING = 2 * P + 4;
 
   const int x0 = blockIdx.x * ZTX, y0 = blockIdx.y * ZBY;
   const int d_hi = d_lo + D - 1;
   const size_t ibase = (size_t)b * H * W;
   // F = image at the fixed column; G = image at the shifted column x -/+ r.
-  const uint8_t* Fimg = TAR ? warped : ref;
-  const uint8_t* Gimg = TAR ? ref : warped;
-  const int32_t* SFg = TAR ? SWg : SLg;
+  const float* Fimg = TAR ? warped : ref;
+  const float* Gimg = TAR ? ref : warped;
+  const float* SFg = TAR ? SWg : SLg;
   const float* iFg = TAR ? invWg : invLg;
-  const int32_t* SGg = TAR ? SLg : SWg;
+  const float* SGg = TAR ? SLg : SWg;
   const float* iGg = TAR ? invLg : invWg;
   // first image column of the (unoriented) G image row / G statistics row
   const int g0 = TAR ? (x0 - P + d_lo) : (x0 - P - d_hi - gm.gpad);
@@ -266,75 +288,82 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
   auto orient_g = [&](int c) { return TAR ? c : gm.RB - c; };
   auto orient_s = [&](int c) { return TAR ? c : gm.RS - c; };
 
-  // ---- row streaming (loads land raw in registers, converted one iteration later) ----
-  // image / statistics elements per thread per row (upper bounds over P <= 7 and the
-  // D this CTA width serves: 64 for ZTX = 64, 16 for ZT_SMALL)
+  // ---- row streaming: 4-byte cp.async copies from the fp32 planes straight into the
+  // ring (oriented, plus the one-entry-shifted copy); columns / rows outside the image
+  // are filled (image and S: 0, norms: NaN).  Copies run two rows ahead of the math.
+  // per-thread trip counts are compile-time upper bounds (P <= 7, the D this CTA width
+  // serves: 64 for ZTX = 64, 32 for ZT_MID, 16 for ZT_SMALL); 128 threads per CTA
+  constexpr int NTHR = 128;
   constexpr int DMAX = ZTX == 64 ? 64 : (ZTX == ZT_MID ? 32 : 16);
-  constexpr int NPI = (2 * ZTX + 4 * 7 + DMAX + 32 + 127) / 128;
-  constexpr int NPS = (4 * ZTX + 2 * DMAX + 40 + 127) / 128;
-  uint32_t pi_[NPI], ps_[NPS];
-  const int NIMG = gm.FC + gm.GC, NSTAT = 2 * ZTX + 2 * gm.SGC;
-  auto fetch = [&](int t_img, int y_st) {
-    const int yy_i = y0 - P + t_img, yy_s = y0 + y_st;
-    const bool row_i = t_img >= 0 && yy_i >= 0 && yy_i < H;
+  constexpr int FCMAX = ((ZTX + 2 * P + 3) / 4) * 4 + 4;
+  constexpr int GCMAX = ((ZTX + 2 * P + DMAX - 1 + 3 + 3) / 4) * 4 + 8;
+  constexpr int SGCMAX = ((ZTX + DMAX - 1 + 3 + 3) / 4) * 4 + 8;
+  constexpr int TF = (FCMAX + NTHR - 1) / NTHR, TG = (GCMAX + NTHR - 1) / NTHR;
+  constexpr int TSF = 2 * ZTX / NTHR, TSG = (2 * SGCMAX + NTHR - 1) / NTHR;
+  static_assert(2 * ZTX % NTHR == 0, "F statistics: whole trips");
+  auto issue_img = [&](int t_img) {
+    const int slot = t_img % NRING;
+    const int yy = y0 - P + t_img;
+    float* fs = Fs + slot * gm.FC;
+    float* gs = Gs + slot * gm.GROW;
+    float* gs1 = Gs1 + slot * gm.GROW;
+    const bool row_in = yy >= 0 && yy < H;   // CTA-uniform
+    const float* frow = Fimg + ibase + (size_t)(row_in ? yy : 0) * W;
+    const float* grow = Gimg + ibase + (size_t)(row_in ? yy : 0) * W;
 #pragma unroll
-    for (int u = 0; u < NPI; u++) {
-      const int e = threadIdx.x + u * 128;
-      const bool isF = e < gm.FC;
-      const int xx = isF ? x0 - P + e : g0 + (e - gm.FC);
-      const uint8_t* img = isF ? Fimg : Gimg;
-      pi_[u] = (row_i && e < NIMG && xx >= 0 && xx < W) ? (uint32_t)__ldg(img + ibase + (size_t)yy_i * W + xx) : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < NPS; u++) {
-      const int k = threadIdx.x + u * 128;
-      uint32_t v = 0u;
-      if (y_st >= 0 && k < NSTAT) {
-        const bool isF = k < 2 * ZTX;
-        const int kk = isF ? k : k - 2 * ZTX;
-        const int per = isF ? ZTX : gm.SGC;
-        const bool isInv = kk >= per;
-        const int xx = (isF ? x0 : s0) + (isInv ? kk - per : kk);
-        const bool in = yy_s < H && xx >= 0 && xx < W;
-        const size_t gi = ibase + (size_t)yy_s * W + xx;
-        if (isInv) v = in ? __float_as_uint(__ldg((isF ? iFg : iGg) + gi)) : 0x7fffffffu;
-        else v = in ? (uint32_t)__ldg((isF ? SFg : SGg) + gi) : 0u;
+    for (int u = 0; u < TF; u++) {
+      const int e = threadIdx.x + u * NTHR;
+      const int xx = x0 - P + e;
+      RSR_CHECK(slot < gm.NRING);
+      if (e < gm.FC) {
+        if (row_in && xx >= 0 && xx < W) cp_async4(fs + e, frow + xx);
+        else fs[e] = 0.f;
       }
-      ps_[u] = v;
     }
-  };
-  // exact integer -> float for 0 <= v < 2^23 without the XU pipe
-  auto u2f = [](uint32_t v) { return __uint_as_float(0x4B000000u | v) - 8388608.0f; };
-  auto commit = [&](int t_img, int y_st) {
-    const int slot = t_img % (2 * P + 3);
-    if (t_img >= 0) {
 #pragma unroll
-      for (int u = 0; u < NPI; u++) {
-        const int e = threadIdx.x + u * 128;
-        if (e < gm.FC) {
-          Fs[slot * gm.FC + e] = u2f(pi_[u]);
-        } else if (e < NIMG) {
-          const int o = orient_g(e - gm.FC);
-          RSR_CHECK(o >= 0 && o < gm.GROW && slot < gm.NRING);
-          const float v = u2f(pi_[u]);
-          Gs[slot * gm.GROW + o] = v;
-          if (o > 0) Gs1[slot * gm.GROW + o - 1] = v;
+    for (int u = 0; u < TG; u++) {
+      const int c = threadIdx.x + u * NTHR;
+      const int xx = g0 + c;
+      const int o = orient_g(c);
+      if (c < gm.GC) {
+        RSR_CHECK(o >= 0 && o < gm.GROW);
+        if (row_in && xx >= 0 && xx < W) {
+          cp_async4(gs + o, grow + xx);
+          if (o > 0) cp_async4(gs1 + o - 1, grow + xx);
+        } else {
+          gs[o] = 0.f;
+          if (o > 0) gs1[o - 1] = 0.f;
         }
       }
     }
-    if (y_st >= 0) {
-      float* st = St + (y_st & 1) * SROW;
+  };
+  auto issue_stats = [&](int y_st) {
+    float* st = St + (y_st % 3) * SROW;
+    const size_t rowo = ibase + (size_t)(y0 + y_st) * W;   // y0 + y_st < H
 #pragma unroll
-      for (int u = 0; u < NPS; u++) {
-        const int k = threadIdx.x + u * 128;
-        if (k < 2 * ZTX) {
-          st[k] = k >= ZTX ? __uint_as_float(ps_[u]) : u2f(ps_[u]);
-        } else if (k < NSTAT) {
-          const int kk = k - 2 * ZTX;
-          const bool isInv = kk >= gm.SGC;
-          const float v = isInv ? __uint_as_float(ps_[u]) : u2f(ps_[u]);
-          const int o = orient_s(isInv ? kk - gm.SGC : kk);
-          float* row = st + 2 * ZTX + (isInv ? 2 : 0) * gm.SROW2;   // sG | sG1 | iG | iG1
+    for (int u = 0; u < TSF; u++) {
+      const int k = threadIdx.x + u * NTHR;
+      const bool isInv = k >= ZTX;
+      const int xx = x0 + (isInv ? k - ZTX : k);
+      if (xx < W) cp_async4(st + k, (isInv ? iFg : SFg) + rowo + xx);
+      else st[k] = isInv ? qnan() : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < TSG; u++) {
+      const int k = threadIdx.x + u * NTHR;
+      if (k < 2 * gm.SGC) {
+        const bool isInv = k >= gm.SGC;
+        const int c = isInv ? k - gm.SGC : k;
+        const int xx = s0 + c;
+        const int o = orient_s(c);
+        RSR_CHECK(o >= 0 && o < gm.SROW2);
+        float* row = st + 2 * ZTX + (isInv ? 2 : 0) * gm.SROW2;   // sG | sG1 | iG | iG1
+        if (xx >= 0 && xx < W) {
+          const float* src = (isInv ? iGg : SGg) + rowo + xx;
+          cp_async4(row + o, src);
+          if (o > 0) cp_async4(row + gm.SROW2 + o - 1, src);
+        } else {
+          const float v = isInv ? qnan() : 0.f;
           row[o] = v;
           if (o > 0) row[gm.SROW2 + o - 1] = v;
         }
@@ -342,11 +371,12 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
     }
   };
 
-  // prologue: image rows 0 .. 2P and the statistics of output row 0
-  for (int t = 0; t <= 2 * P; t++) {
-    fetch(t, t == 0 ? 0 : -1);
-    commit(t, t == 0 ? 0 : -1);
-  }
+  // prologue: image rows 0 .. 2P + 1 and the statistics of output rows 0 and 1
+  for (int t = 0; t <= 2 * P + 1; t++) issue_img(t);
+  issue_stats(0);
+  if (nrows > 1) issue_stats(1);
+  cp_async_commit();
+  cp_async_wait_all();
   __syncthreads();
 
   const int n_rg = (D + ZR - 1) / ZR;
@@ -370,7 +400,7 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
     for (int qp = 0; qp < NQP; qp++) V2[j][qp] = make_float2(0.f, 0.f);
 
   auto accumulate_row = [&](int t, bool subtract) {
-    const int slot = t % (2 * P + 3);
+    const int slot = t % NRING;
     float f[NF4 * 4], ge[NG4 * 4], go[NG4 * 4];
     RSR_CHECK(slot < gm.NRING && f_start + NF4 * 4 <= gm.FC && grun >= 0 && grun + NG4 * 4 <= gm.GROW);
     const float4* fr = reinterpret_cast<const float4*>(Fs + slot * gm.FC + f_start);
@@ -402,9 +432,12 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
   };
 
   for (int y = 0; y < nrows; y++) {
-    // prefetch image row y + 1 + 2P and the statistics of output row y + 1
-    const bool more = y + 1 < nrows;
-    if (more) fetch(y + 1 + 2 * P, y + 1);
+    // copies for iteration y + 2: image row y + 2 + 2P, statistics of output row y + 2
+    if (y + 2 < nrows) {
+      issue_img(y + 2 + 2 * P);
+      issue_stats(y + 2);
+    }
+    cp_async_commit();
     if (active) {
       if (y == 0) {
 #pragma unroll 1
@@ -414,7 +447,7 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
         accumulate_row(y - 1, true);
       }
       // block statistics of this row: F side per pixel, G side as oriented pairs
-      const float* st = St + (y & 1) * SROW;
+      const float* st = St + (y % 3) * SROW;
       float sF[ZX], iF[ZX], sGe[NS4 * 4], sGo[NS4 * 4], iGe[NS4 * 4], iGo[NS4 * 4];
       {
         const float4 a = *reinterpret_cast<const float4*>(st + ZX * cg);
@@ -517,9 +550,10 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
         }
       }
     }
-    // the ring slot of row y - 2 and St[(y + 1) & 1] were last read in iteration
-    // y - 1, which every thread finished before the previous barrier
-    if (more) commit(y + 1 + 2 * P, y + 1);
+    // this thread's copies for iteration y + 1 have landed; the barrier publishes
+    // everyone's (the slot of row y - 2 and St[(y + 2) % 3], written by the copies
+    // issued above, were last read in iteration y - 1)
+    cp_async_wait_prev();
     __syncthreads();
   }
 }
@@ -527,9 +561,9 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
 #define RSR_ZNCC_BOUNDS __launch_bounds__(128, (P <= 3 ? 3 : (P <= 5 ? 2 : 1)))
 
 template <int P, bool TAR>
-__global__ void RSR_ZNCC_BOUNDS k_zncc(int H, int W, int d_lo, int D, int Dst, int koff, const uint8_t* ref,
-                                       const uint8_t* warped, const int32_t* SLg, const float* invLg,
-                                       const int32_t* SWg, const float* invWg, float* vol) {
+__global__ void RSR_ZNCC_BOUNDS k_zncc(int H, int W, int d_lo, int D, int Dst, int koff, const float* ref,
+                                       const float* warped, const float* SLg, const float* invLg,
+                                       const float* SWg, const float* invWg, float* vol) {
   zncc_cta<P, TAR>(blockIdx.z, H, W, d_lo, D, Dst, koff, ref, warped, SLg, invLg, SWg, invWg, vol);
 }
 
@@ -539,8 +573,8 @@ __global__ void RSR_ZNCC_BOUNDS k_zncc(int H, int W, int d_lo, int D, int Dst, i
 template <int P, int ZT>
 __global__ void __launch_bounds__(128, (ZT != ZT_SMALL ? (P <= 3 ? 3 : (P <= 5 ? 2 : 1)) : (P <= 5 ? 2 : 1)))
     k_zncc_pair(int B, int H, int W, int d_lo, int D, int Dst, int koff,
-                                            const uint8_t* ref, const uint8_t* warped, const int32_t* SLg,
-                                            const float* invLg, const int32_t* SWg, const float* invWg,
+                                            const float* ref, const float* warped, const float* SLg,
+                                            const float* invLg, const float* SWg, const float* invWg,
                                             float* vol_ref, float* vol_tar) {
   if ((int)blockIdx.z < B)
     zncc_cta<P, false, ZT>(blockIdx.z, H, W, d_lo, D, Dst, koff, ref, warped, SLg, invLg, SWg, invWg, vol_ref);
@@ -549,9 +583,9 @@ __global__ void __launch_bounds__(128, (ZT != ZT_SMALL ? (P <= 3 ? 3 : (P <= 5 ?
 }
 
 template <int P, int ZT>
-static cudaError_t zncc_pair_launch_zt(int B, int H, int W, int d_lo, int D, int Dst, int koff, const uint8_t* ref,
-                                       const uint8_t* warped, const int32_t* SL, const float* invL,
-                                       const int32_t* SW, const float* invW, float* vol_ref, float* vol_tar,
+static cudaError_t zncc_pair_launch_zt(int B, int H, int W, int d_lo, int D, int Dst, int koff, const float* ref,
+                                       const float* warped, const float* SL, const float* invL,
+                                       const float* SW, const float* invW, float* vol_ref, float* vol_tar,
                                        cudaStream_t st) {
   const size_t smem = zncc_smem(P, D, ZT);
   auto kern = k_zncc_pair<P, ZT>;
@@ -564,18 +598,18 @@ static cudaError_t zncc_pair_launch_zt(int B, int H, int W, int d_lo, int D, int
 
 // Both volumes from the reference CTAs alone (SHEAR): grid of B frames
 template <int P>
-__global__ void RSR_ZNCC_BOUNDS k_zncc_shear(int H, int W, int d_lo, int D, int Dst, int koff, const uint8_t* ref,
-                                             const uint8_t* warped, const int32_t* SLg, const float* invLg,
-                                             const int32_t* SWg, const float* invWg, float* vol_ref,
+__global__ void RSR_ZNCC_BOUNDS k_zncc_shear(int H, int W, int d_lo, int D, int Dst, int koff, const float* ref,
+                                             const float* warped, const float* SLg, const float* invLg,
+                                             const float* SWg, const float* invWg, float* vol_ref,
                                              float* vol_tar) {
   zncc_cta<P, false, ZTX, true>(blockIdx.z, H, W, d_lo, D, Dst, koff, ref, warped, SLg, invLg, SWg, invWg, vol_ref,
                                 vol_tar);
 }
 
 template <int P>
-static cudaError_t zncc_shear_launch_t(int B, int H, int W, int d_lo, int D, int Dst, int koff, const uint8_t* ref,
-                                       const uint8_t* warped, const int32_t* SL, const float* invL,
-                                       const int32_t* SW, const float* invW, float* vol_ref, float* vol_tar,
+static cudaError_t zncc_shear_launch_t(int B, int H, int W, int d_lo, int D, int Dst, int koff, const float* ref,
+                                       const float* warped, const float* SL, const float* invL,
+                                       const float* SW, const float* invW, float* vol_ref, float* vol_tar,
                                        cudaStream_t st) {
   const size_t smem = zncc_smem(P, D, ZTX, true);
   auto kern = k_zncc_shear<P>;
@@ -587,9 +621,9 @@ static cudaError_t zncc_shear_launch_t(int B, int H, int W, int d_lo, int D, int
 }
 
 template <int P>
-static cudaError_t zncc_pair_launch_t(int B, int H, int W, int d_lo, int D, int Dst, int koff, const uint8_t* ref,
-                                      const uint8_t* warped, const int32_t* SL, const float* invL,
-                                      const int32_t* SW, const float* invW, float* vol_ref, float* vol_tar,
+static cudaError_t zncc_pair_launch_t(int B, int H, int W, int d_lo, int D, int Dst, int koff, const float* ref,
+                                      const float* warped, const float* SL, const float* invL,
+                                      const float* SW, const float* invW, float* vol_ref, float* vol_tar,
                                       cudaStream_t st) {
   if (zncc_cta_cols(D) == ZT_SMALL)
     return zncc_pair_launch_zt<P, ZT_SMALL>(B, H, W, d_lo, D, Dst, koff, ref, warped, SL, invL, SW, invW,
@@ -610,9 +644,9 @@ static cudaError_t zncc_pair_launch_t(int B, int H, int W, int d_lo, int D, int 
 
 template <int P, bool TAR>
 static cudaError_t zncc_launch_t(int B, int H, int W, int d_lo, int D, int Dst, int koff,
-                                 const uint8_t* ref,
-                                 const uint8_t* warped, const int32_t* SL, const float* invL,
-                                 const int32_t* SW, const float* invW, float* vol,
+                                 const float* ref,
+                                 const float* warped, const float* SL, const float* invL,
+                                 const float* SW, const float* invW, float* vol,
                                  cudaStream_t st) {
   const size_t smem = zncc_smem(P, D);
   auto kern = k_zncc<P, TAR>;
@@ -714,8 +748,8 @@ cudaError_t launch_nan_maps(int B, int H, int W, int d_lo, int D, const float* i
   return cudaGetLastError();
 }
 
-cudaError_t launch_zncc_pair(int B, int H, int W, int rho_b, int d_lo, int D, const uint8_t* ref,
-                             const uint8_t* warped, const int32_t* SL, const float* invL, const int32_t* SW,
+cudaError_t launch_zncc_pair(int B, int H, int W, int rho_b, int d_lo, int D, const float* ref,
+                             const float* warped, const float* SL, const float* invL, const float* SW,
                              const float* invW, float* vol_ref, float* vol_tar, cudaStream_t st) {
   constexpr int SLAB = 64;
   if (2LL * B > 65535) return cudaErrorInvalidValue;
@@ -740,8 +774,8 @@ cudaError_t launch_zncc_pair(int B, int H, int W, int rho_b, int d_lo, int D, co
 }
 
 cudaError_t launch_zncc(bool tar, int B, int H, int W, int rho_b, int d_lo, int D,
-                        const uint8_t* ref, const uint8_t* warped, const int32_t* SL,
-                        const float* invL, const int32_t* SW, const float* invW, float* vol,
+                        const float* ref, const float* warped, const float* SL,
+                        const float* invL, const float* SW, const float* invW, float* vol,
                         cudaStream_t st) {
   // Disparity slabs of at most 64 (<= 128 threads per CTA).
   constexpr int SLAB = 64;
