@@ -129,6 +129,94 @@ __global__ void __launch_bounds__(256) k_block_stats(int B, int H, int W,
   }
 }
 
+// Column-sliding block statistics for rsr_cost_volume (uint8 images, fp32 outputs as
+// in k_block_stats<FOUT>, same integers and the same single rounding per value).  A
+// thread owns one tile column and slides the vertical (2P+1)-sums of i, i^2 and the
+// mask down BS_BY output rows (the entering row prefetched one row ahead, the leaving
+// row re-read from L1); per output row the vertical sums go to
+// a double-buffered shared row and the horizontal (2P+1)-sums are read back: one CTA
+// barrier per row, one 8-byte load per tap.  Frames [0, B) are img0, [B, 2B) img1.
+constexpr int BS_BX = 128, BS_BY = 48;
+
+template <int P>
+__global__ void __launch_bounds__(160) k_block_stats_col(int B, int H, int W,
+                                                         const uint8_t* __restrict__ img0,
+                                                         const uint8_t* __restrict__ mask0, float* __restrict__ S0,
+                                                         float* __restrict__ inv0, float* __restrict__ F0,
+                                                         const uint8_t* __restrict__ img1,
+                                                         const uint8_t* __restrict__ mask1, float* __restrict__ S1,
+                                                         float* __restrict__ inv1, float* __restrict__ F1) {
+  constexpr int NR = 2 * P + 1, TC = BS_BX + 2 * P;
+  static_assert(TC <= 160, "one thread per tile column");
+  __shared__ int2 vs[2][TC];   // (S * 256 + M, S2): vertical sums of the tile columns
+  __shared__ int cp[2][TC];    // centre pixel of the row
+  const bool second = (int)blockIdx.z >= B;
+  const int b = second ? (int)blockIdx.z - B : (int)blockIdx.z;
+  const uint8_t* __restrict__ img = second ? img1 : img0;
+  const uint8_t* __restrict__ mask = second ? mask1 : mask0;
+  float* __restrict__ Sout = second ? S1 : S0;
+  float* __restrict__ inv = second ? inv1 : inv0;
+  float* __restrict__ Fout = second ? F1 : F0;
+  const int t = threadIdx.x;
+  const int x0 = blockIdx.x * BS_BX, y0 = blockIdx.y * BS_BY;
+  const int xx = x0 - P + t;
+  const bool col_in = t < TC && xx >= 0 && xx < W;
+  const size_t base = (size_t)b * H * W;
+  auto load = [&](int yy, int& pv, int& mv) {
+    pv = 0; mv = 0;
+    if (col_in && yy >= 0 && yy < H) {
+      const size_t g = base + (size_t)yy * W + xx;
+      pv = __ldg(img + g);
+      mv = mask ? (__ldg(mask + g) != 0) : 1;
+    }
+  };
+  int vs1 = 0, vs2 = 0, vm = 0;
+  for (int k = 0; k < NR - 1; k++) {   // rows y0 - P .. y0 + P - 1
+    int pv, mv;
+    load(y0 - P + k, pv, mv);
+    vs1 += pv; vs2 += pv * pv; vm += mv;
+  }
+  int np, nm;
+  load(y0 + P, np, nm);
+  const int yend = min(H, y0 + BS_BY);
+  const int n = NR * NR;
+  // (entering rows prefetched 6 rows ahead through a register ring measured slower:
+  // 131 vs 104 us per c5 batch)
+  for (int yc = y0; yc < yend; yc++) {
+    // the entering row yc + P was prefetched; the leaving row yc - P and the centre
+    // row yc are re-read (L1 hits: loaded 2P + 1 and P rows ago)
+    int op, om, cpv, cmv;
+    load(yc - P, op, om);
+    load(yc, cpv, cmv);
+    vs1 += np; vs2 += np * np; vm += nm;
+    load(yc + P + 1, np, nm);                // prefetch the next entering row
+    const int buf = yc & 1;
+    if (t < TC) {
+      vs[buf][t] = make_int2(vs1 * 256 + vm, vs2);
+      cp[buf][t] = cpv;
+    }
+    vs1 -= op; vs2 -= op * op; vm -= om;
+    __syncthreads();
+    const int xo = x0 + t;
+    if (t < BS_BX && xo < W) {
+      int a = 0, s2 = 0;
+#pragma unroll
+      for (int d = 0; d < NR; d++) {
+        const int2 v = vs[buf][t + d];
+        a += v.x; s2 += v.y;
+      }
+      const int s1 = a >> 8, m = a & 255;
+      const bool inside = yc >= P && yc <= H - 1 - P && xo >= P && xo <= W - 1 - P;
+      const long long var = (long long)n * s2 - (long long)s1 * s1;
+      const bool ok = inside && m == n && var != 0;
+      const size_t g = base + (size_t)yc * W + xo;
+      Sout[g] = (float)s1;
+      inv[g] = ok ? rsqrtf((float)var) : qnan();
+      Fout[g] = (float)cp[buf][t + P];
+    }
+  }
+}
+
 template <typename T1, bool FOUT = false>
 static cudaError_t block_stats_t(int B, int H, int W, int rho_b, const uint8_t* img0, const uint8_t* mask0,
                                  int32_t* S0, float* inv0, const T1* img1, const uint8_t* mask1, int32_t* S1,
@@ -165,8 +253,22 @@ cudaError_t launch_block_stats(int B, int H, int W, int rho_b, const uint8_t* im
 cudaError_t launch_block_stats_f(int B, int H, int W, int rho_b, const uint8_t* img0, const uint8_t* mask0,
                                  float* S0, float* inv0, float* F0, const uint8_t* img1, const uint8_t* mask1,
                                  float* S1, float* inv1, float* F1, cudaStream_t st) {
-  return block_stats_t<uint8_t, true>(B, H, W, rho_b, img0, mask0, reinterpret_cast<int32_t*>(S0), inv0, img1,
-                                      mask1, reinterpret_cast<int32_t*>(S1), inv1, st, F0, F1);
+  if (const char* e = getenv("RSR_BS_TILE"); e && e[0] == '1')   // A/B hook (tools/): the tiled kernel
+    return block_stats_t<uint8_t, true>(B, H, W, rho_b, img0, mask0, reinterpret_cast<int32_t*>(S0), inv0, img1,
+                                        mask1, reinterpret_cast<int32_t*>(S1), inv1, st, F0, F1);
+  const int nimg = img1 ? 2 : 1;
+  if ((long long)nimg * B > 65535) return cudaErrorInvalidValue;
+  dim3 grid((W + BS_BX - 1) / BS_BX, (H + BS_BY - 1) / BS_BY, nimg * B);
+  switch (rho_b) {
+#define RSR_BSC(PP)                                                                                       \
+  case PP:                                                                                                \
+    k_block_stats_col<PP><<<grid, 160, 0, st>>>(B, H, W, img0, mask0, S0, inv0, F0, img1, mask1, S1, inv1, F1); \
+    break;
+    RSR_BSC(1) RSR_BSC(2) RSR_BSC(3) RSR_BSC(4) RSR_BSC(5) RSR_BSC(6) RSR_BSC(7)
+#undef RSR_BSC
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_block_stats16(int B, int H, int W, int rho_b, const uint8_t* img0, int32_t* S0, float* inv0,
@@ -738,9 +840,86 @@ __global__ void __launch_bounds__(256) k_nan_maps(int H, int W, int d_lo, int D,
   }
 }
 
+// The same summaries with one warp per (row, frame), NM_WARPS rows per CTA and no CTA
+// barrier: finite flags are staged coalesced, each lane scans a contiguous chunk of
+// odd length (conflict-free), the chunk totals are combined by a warp scan.
+constexpr int NM_WARPS = 4;
+__global__ void __launch_bounds__(32 * NM_WARPS) k_nan_maps_warp(int B, int H, int W, int d_lo, int D,
+                                                                 const float* __restrict__ invL,
+                                                                 const float* __restrict__ invW,
+                                                                 uint8_t* __restrict__ nan_ref,
+                                                                 uint8_t* __restrict__ nan_tar) {
+  extern __shared__ int nmw_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long r = (long long)blockIdx.x * NM_WARPS + warp;   // row of the batch
+  if (r >= (long long)B * H) return;                             // whole warp
+  int* cL = nmw_smem + (size_t)warp * 2 * (W + 1);   // [W + 1] prefix counts of finite inv_L
+  int* cW = cL + (W + 1);                           // [W + 1] prefix counts of finite inv_W
+  const size_t row = (size_t)r * W;
+  for (int c = lane; c < W; c += 32) {
+    const float a = invL[row + c], w = invW[row + c];
+    cL[c + 1] = a == a;
+    cW[c + 1] = w == w;
+  }
+  if (lane == 0) { cL[0] = 0; cW[0] = 0; }
+  __syncwarp();
+  const int chunk = ((W + 31) / 32) | 1;
+  const int c0 = min(W, lane * chunk), c1 = min(W, c0 + chunk);
+  int sl = 0, sw = 0;
+  for (int c = c0; c < c1; c++) { sl += cL[c + 1]; sw += cW[c + 1]; }
+  int il = sl, iw = sw;   // inclusive warp scan of the chunk totals
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int tl = __shfl_up_sync(0xffffffffu, il, o), tw = __shfl_up_sync(0xffffffffu, iw, o);
+    if (lane >= o) { il += tl; iw += tw; }
+  }
+  int rl = il - sl, rw = iw - sw;
+  for (int c = c0; c < c1; c++) {
+    rl += cL[c + 1]; rw += cW[c + 1];
+    cL[c + 1] = rl; cW[c + 1] = rw;
+  }
+  __syncwarp();
+  auto count = [&](const int* cnt, int a, int bcol) {   // finite entries in columns [a, b]
+    a = max(a, 0);
+    bcol = min(bcol, W - 1);
+    return bcol < a ? 0 : cnt[bcol + 1] - cnt[a];
+  };
+  const bool halves = D <= 64;
+  const int H0 = min(((D + 7) & ~7) / 2, D);
+  for (int u = lane; u < W; u += 32) {
+    const bool lok = cL[u + 1] - cL[u] != 0, wok = cW[u + 1] - cW[u] != 0;
+    if (nan_ref) {   // k valid iff inv_L(u) and inv_W(u - d_lo - k) finite
+      const int f0 = lok ? count(cW, u - d_lo - (H0 - 1), u - d_lo) : 0;
+      const int f1 = lok ? count(cW, u - d_lo - (D - 1), u - d_lo - H0) : 0;
+      const int fin = f0 + f1;
+      int m = (fin < D ? 1 : 0) | (fin > 0 ? 2 : 0);
+      if (halves) m |= (f0 < H0 ? 4 : 0) | (f1 < D - H0 ? 8 : 0) | 0x80;
+      nan_ref[row + u] = (uint8_t)m;
+    }
+    if (nan_tar) {   // k valid iff inv_W(u') and inv_L(u' + d_lo + k) finite
+      const int f0 = wok ? count(cL, u + d_lo, u + d_lo + H0 - 1) : 0;
+      const int f1 = wok ? count(cL, u + d_lo + H0, u + d_lo + D - 1) : 0;
+      const int fin = f0 + f1;
+      int m = (fin < D ? 1 : 0) | (fin > 0 ? 2 : 0);
+      if (halves) m |= (f0 < H0 ? 4 : 0) | (f1 < D - H0 ? 8 : 0) | 0x80;
+      nan_tar[row + u] = (uint8_t)m;
+    }
+  }
+}
+
 cudaError_t launch_nan_maps(int B, int H, int W, int d_lo, int D, const float* invL,
                             const float* invW, uint8_t* nan_ref, uint8_t* nan_tar, cudaStream_t st) {
   if (!nan_ref && !nan_tar) return cudaSuccess;
+  const size_t smem_w = sizeof(int) * 2 * ((size_t)W + 1) * NM_WARPS;
+  const long long rows = (long long)B * H;
+  if (smem_w <= 227 * 1024 && (rows + NM_WARPS - 1) / NM_WARPS <= 0x7fffffffLL &&
+      !(getenv("RSR_NM_CTA") && getenv("RSR_NM_CTA")[0] == '1')) {   // A/B hook (tools/): per-row CTAs
+    const cudaError_t e = smem_optin((const void*)k_nan_maps_warp, smem_w);
+    if (e != cudaSuccess) return e;
+    k_nan_maps_warp<<<(unsigned)((rows + NM_WARPS - 1) / NM_WARPS), 32 * NM_WARPS, smem_w, st>>>(
+        B, H, W, d_lo, D, invL, invW, nan_ref, nan_tar);
+    return cudaGetLastError();
+  }
   const size_t smem = sizeof(int) * 2 * ((size_t)W + 1);
   const cudaError_t e = smem_optin((const void*)k_nan_maps, smem);
   if (e != cudaSuccess) return e;
