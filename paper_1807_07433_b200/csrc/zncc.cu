@@ -550,26 +550,15 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
       }
       // block statistics of this row: F side per pixel, G side as oriented pairs
       const float* st = St + (y % 3) * SROW;
-      float sF[ZX], iF[ZX], sGe[NS4 * 4], sGo[NS4 * 4], iGe[NS4 * 4], iGo[NS4 * 4];
-      {
-        const float4 a = *reinterpret_cast<const float4*>(st + ZX * cg);
-        const float4 c = *reinterpret_cast<const float4*>(st + ZTX + ZX * cg);
-        sF[0] = a.x; sF[1] = a.y; sF[2] = a.z; sF[3] = a.w;
-        iF[0] = c.x; iF[1] = c.y; iF[2] = c.z; iF[3] = c.w;
-        RSR_CHECK(srun >= 0 && srun + NS4 * 4 <= gm.SROW2 && ZX * cg + ZX <= ZTX);
-        const float* sg = st + 2 * ZTX + srun;
-#pragma unroll
-        for (int i = 0; i < NS4; i++) {
-          const float4 t0 = reinterpret_cast<const float4*>(sg)[i];
-          const float4 t1 = reinterpret_cast<const float4*>(sg + gm.SROW2)[i];
-          const float4 t2 = reinterpret_cast<const float4*>(sg + 2 * gm.SROW2)[i];
-          const float4 t3 = reinterpret_cast<const float4*>(sg + 3 * gm.SROW2)[i];
-          sGe[4 * i] = t0.x; sGe[4 * i + 1] = t0.y; sGe[4 * i + 2] = t0.z; sGe[4 * i + 3] = t0.w;
-          sGo[4 * i] = t1.x; sGo[4 * i + 1] = t1.y; sGo[4 * i + 2] = t1.z; sGo[4 * i + 3] = t1.w;
-          iGe[4 * i] = t2.x; iGe[4 * i + 1] = t2.y; iGe[4 * i + 2] = t2.z; iGe[4 * i + 3] = t2.w;
-          iGo[4 * i] = t3.x; iGo[4 * i + 1] = t3.y; iGo[4 * i + 2] = t3.z; iGo[4 * i + 3] = t3.w;
-        }
-      }
+      float sF[ZX], iF[ZX];
+      const float4 sfa = *reinterpret_cast<const float4*>(st + ZX * cg);
+      const float4 ifa = *reinterpret_cast<const float4*>(st + ZTX + ZX * cg);
+      sF[0] = sfa.x; sF[1] = sfa.y; sF[2] = sfa.z; sF[3] = sfa.w;
+      iF[0] = ifa.x; iF[1] = ifa.y; iF[2] = ifa.z; iF[3] = ifa.w;
+      RSR_CHECK(srun >= 0 && srun + NS4 * 4 <= gm.SROW2 && ZX * cg + ZX <= ZTX);
+      // G-side statistics are read per pixel (8 oriented entries from the even or the
+      // shifted copy), not held for all ZX pixels: 32 fewer live registers
+      const float* sg = st + 2 * ZTX + srun;
       const int yy = y0 + y;
       float* vrow = vol + ((ibase + (size_t)yy * W) * Dst) + koff;
       // NaN structure from the statistics alone (num is always finite): c(i, q) is NaN
@@ -597,16 +586,18 @@ __device__ __forceinline__ void zncc_cta(int b, int H, int W, int d_lo, int D, i
 #pragma unroll
         for (int qp = 0; qp < NQP; qp++) {
           const int o = oi + 2 * qp;
-          const float2 sg = (o & 1) ? make_float2(sGo[o - 1], sGo[o]) : make_float2(sGe[o], sGe[o + 1]);
-          const float2 ig = (o & 1) ? make_float2(iGo[o - 1], iGo[o]) : make_float2(iGe[o], iGe[o + 1]);
+          // (o & 1) == (oi & 1): the pair starts at an even entry of sG (oi even) or sG1
+          const float2 sgv = *reinterpret_cast<const float2*>((o & 1) ? sg + gm.SROW2 + o - 1 : sg + o);
+          const float2 ig = *reinterpret_cast<const float2*>((o & 1) ? sg + 3 * gm.SROW2 + o - 1
+                                                                       : sg + 2 * gm.SROW2 + o);
           const float2 sf = make_float2(sF[i], sF[i]), inf = make_float2(iF[i], iF[i]);
           const float2 nn = make_float2(nf, nf);
           // n S_lw - S_l S_w: the product S_l S_w split error-free (bb + be), then one
           // FMA forms n S_lw - bb exactly rounded; exact whenever |num| < 2^24 - 8
           // (cancellation), 1e-7 relative otherwise
-          const float2 bb = f2mul(sf, sg);
+          const float2 bb = f2mul(sf, sgv);
           const float2 nbb = make_float2(-bb.x, -bb.y);
-          const float2 be = f2fma(sf, sg, nbb);
+          const float2 be = f2fma(sf, sgv, nbb);
           const float2 num = f2sub(f2fma(nn, hs[qp], nbb), be);
           // (num * inv_L) * inv_W, in this order for both volumes (bitwise dual identity)
           const float2 c = TAR ? f2mul(f2mul(num, ig), inf) : f2mul(f2mul(num, inf), ig);
@@ -673,7 +664,12 @@ __global__ void RSR_ZNCC_BOUNDS k_zncc(int H, int W, int d_lo, int D, int Dst, i
 // grid twice as long, so the two halves fill each other's last wave.
 // the wide small-D CTA holds more prefetch registers: two CTAs per SM at most
 template <int P, int ZT>
-__global__ void __launch_bounds__(128, (ZT != ZT_SMALL ? (P <= 3 ? 3 : (P <= 5 ? 2 : 1)) : (P <= 5 ? 2 : 1)))
+#ifdef RSR_K2_MINB4   // experiment build (tools/): four CTAs per SM at P <= 3 (128 registers)
+#define RSR_K2_MB3 4
+#else
+#define RSR_K2_MB3 3
+#endif
+__global__ void __launch_bounds__(128, (ZT != ZT_SMALL ? (P <= 3 ? RSR_K2_MB3 : (P <= 5 ? 2 : 1)) : (P <= 5 ? 2 : 1)))
     k_zncc_pair(int B, int H, int W, int d_lo, int D, int Dst, int koff,
                                             const float* ref, const float* warped, const float* SLg,
                                             const float* invLg, const float* SWg, const float* invWg,
