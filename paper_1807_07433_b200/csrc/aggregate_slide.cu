@@ -275,14 +275,22 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
   constexpr int NAB = (NT + 3) / 4;          // age blocks of 4
   const int NR = (s.yb - s.ya) + 2 * RHO;
   const int xs = lane >> 2, as = lane & 3;
-  float sreg[NAB][NT];   // exp2(kd (dx^2 + dy^2)) for this lane's ages
-#pragma unroll
-  for (int n = 0; n < NAB; n++) {
+  // exp2(kd (dx^2 + dy^2)) for this lane's ages: items (n, n + 1) as packed pairs (the
+  // range-table path multiplies and sums two items per FMUL2 / FADD2), an odd last item
+  constexpr int NP = NAB / 2;
+  float2 sp[NP > 0 ? NP : 1][NT];
+  float ss[NT];
+  auto sfac = [&](int n, int j) {
     const int a = min(n * 4 + as, NT - 1);
+    return ex2_ftz((float)((j - RHO) * (j - RHO) + (RHO - a) * (RHO - a)) * A.kd);
+  };
 #pragma unroll
-    for (int j = 0; j < NT; j++)
-      sreg[n][j] = ex2_ftz((float)((j - RHO) * (j - RHO) + (RHO - a) * (RHO - a)) * A.kd);
+  for (int j = 0; j < NT; j++) {
+#pragma unroll
+    for (int q = 0; q < NP; q++) sp[q][j] = make_float2(sfac(2 * q, j), sfac(2 * q + 1, j));
+    ss[j] = (NAB & 1) ? sfac(NAB - 1, j) : 0.f;
   }
+  auto sreg = [&](int n, int j) { return (NAB & 1) && n == NAB - 1 ? ss[j] : ((n & 1) ? sp[n >> 1][j].y : sp[n >> 1][j].x); };
   const bool cpa = stage_cpasync(A.D, g);
   for (int pass = 0; pass < npass; pass++) {
     // warp p owns the columns 8p .. 8p + 7 (every age): its running sums are its own
@@ -310,46 +318,80 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
       int gq[NT];
 #pragma unroll
       for (int j = 0; j < NT; j++) gq[j] = trs[p * 8 + xs + j];
+      const int x = p * 8 + xs;
+      RSR_CHECK((i + RHO) < g.GR && x + 2 * RHO < g.CX);
+      int gp[NAB];
+      float* slot[NAB];
+      float d[NAB], w[NAB][NT];
 #pragma unroll
       for (int n = 0; n < NAB; n++) {
-        const int x = p * 8 + xs, a = n * 4 + as;
-        const int ac = min(a, NT - 1);
-        RSR_CHECK((i + ac) < g.GR && (i + RHO) < g.GR && x + 2 * RHO < g.CX);
-        int gp = gt[(i + ac) * g.CX + x + RHO];
-        float* slot = dsum + ((i + ac) % NT) * 32 + x;
-        float d = *slot;
-        float w[NT];
-        if (G16) {
-          // 8.8 fixed-point guide: range factor exp2(kr (dg / 256)^2) on the MUFU pipe,
-          // zero for skipped pixels (the tap's or the centre's)
-          const bool pskip = gp == gskip<G16>();
+        const int ac = min(n * 4 + as, NT - 1);
+        RSR_CHECK((i + ac) < g.GR);
+        gp[n] = gt[(i + ac) * g.CX + x + RHO];
+        slot[n] = dsum + ((i + ac) % NT) * 32 + x;
+        d[n] = *slot[n];
+      }
+      if (G16) {
+        // 8.8 fixed-point guide: range factor exp2(kr (dg / 256)^2) on the MUFU pipe,
+        // zero for skipped pixels (the tap's or the centre's)
+#pragma unroll
+        for (int n = 0; n < NAB; n++) {
+          const bool pskip = gp[n] == gskip<G16>();
 #pragma unroll
           for (int j = 0; j < NT; j++) {
-            const float dg = (float)(gq[j] - gp);
-            w[j] = (pskip || gq[j] == gskip<G16>()) ? 0.f : sreg[n][j] * ex2_ftz(A.kr * (dg * dg));
-          }
-        } else {
-          gp = (gp == SG_GSKIP) ? -SG_GSKIP : gp;
-#pragma unroll
-          for (int j = 0; j < NT; j++) {
-            const int ix = min(gq[j] - gp + 255, SG_RLUT - 1);
-            RSR_CHECK(ix >= 0 && ix < SG_RLUT);
-            w[j] = sreg[n][j] * rlut[ix * RC];   // rlut: this lane's copy
+            const float dg = (float)(gq[j] - gp[n]);
+            w[n][j] = (pskip || gq[j] == gskip<G16>()) ? 0.f : sreg(n, j) * ex2_ftz(A.kr * (dg * dg));
+            d[n] += w[n][j];
           }
         }
+      } else {
+        float r[NAB][NT];
+#pragma unroll
+        for (int n = 0; n < NAB; n++) {
+          const int gpn = (gp[n] == SG_GSKIP) ? -SG_GSKIP : gp[n];
+#pragma unroll
+          for (int j = 0; j < NT; j++) {
+            const int ix = min(gq[j] - gpn + 255, SG_RLUT - 1);
+            RSR_CHECK(ix >= 0 && ix < SG_RLUT);
+            r[n][j] = rlut[ix * RC];   // rlut: this lane's copy
+          }
+        }
+        // w = S * R and the running sums in tap order, two items per packed op (the
+        // same two IEEE roundings as the scalar FMUL / FADD)
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+          float2 d2 = make_float2(d[2 * q], d[2 * q + 1]);
+#pragma unroll
+          for (int j = 0; j < NT; j++) {
+            const float2 w2 = f2mul(sp[q][j], make_float2(r[2 * q][j], r[2 * q + 1][j]));
+            w[2 * q][j] = w2.x;
+            w[2 * q + 1][j] = w2.y;
+            d2 = f2add(d2, w2);
+          }
+          d[2 * q] = d2.x;
+          d[2 * q + 1] = d2.y;
+        }
+        if (NAB & 1) {
+#pragma unroll
+          for (int j = 0; j < NT; j++) {
+            w[NAB - 1][j] = ss[j] * r[NAB - 1][j];
+            d[NAB - 1] += w[NAB - 1][j];
+          }
+        }
+      }
+#pragma unroll
+      for (int n = 0; n < NAB; n++) {
+        const int a = n * 4 + as;
         if (a < NT) {
           float* wd = wst + x * g.XS + a;
           RSR_CHECK(x * g.XS + a + (NT - 1) * 16 < 32 * g.XS && a < 16);
 #pragma unroll
-          for (int j = 0; j < NT; j++) {
-            wd[j * 16] = w[j];
-            d += w[j];
-          }
+          for (int j = 0; j < NT; j++) wd[j * 16] = w[n][j];
           if (a == 0) {   // the output row completing at input row i
-            wst[32 * g.XS + x] = d;
-            *slot = 0.f;
+            wst[32 * g.XS + x] = d[n];
+            *slot[n] = 0.f;
           } else {
-            *slot = d;
+            *slot[n] = d[n];
           }
         }
       }
