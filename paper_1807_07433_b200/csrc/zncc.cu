@@ -296,7 +296,11 @@ constexpr int ZT_SMALL = 256;
 // (a 128-column CTA for 16 < D <= 32 was measured slower at the paper's D = 30:
 // 1.64 vs 1.47 ms per 8 cP frames)
 constexpr int ZT_MID = 128;
+#ifdef RSR_K2_MID   // experiment build (tools/): 128-column CTAs for 16 < D <= 32
+__host__ __device__ constexpr int zncc_cta_cols(int D) { return D <= 16 ? ZT_SMALL : (D <= 32 ? ZT_MID : ZTX); }
+#else
 __host__ __device__ constexpr int zncc_cta_cols(int D) { return D <= 16 ? ZT_SMALL : ZTX; }
+#endif
 constexpr int ZBY = 72;   // output rows per CTA (measured: 72 beats 48/60/80/90/96/144 at c5)
 
 // Shared-memory rows are stored "oriented": the G-side image row and G-side
