@@ -313,6 +313,9 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
       // for the whole kernel (sreg), range factor from a shared table indexed by the
       // integer guide difference (skipped pixels index the zero tail of the table).
       const unsigned short* trs = gt + (i + RHO) * g.CX;   // tap row r
+#ifdef RSR_EXP_NOWCOMP   // experiment build (tools/k3_exp.sh): weights not computed (timing only)
+      if (i >= 0) { __syncwarp(); mbar_arrive(&full_w[st]); continue; }
+#endif
       // the tap row's guide values of this lane's column, loaded once for its NAB items
       // (reloaded per item otherwise: the item's stores may alias the tile)
       int gq[NT];

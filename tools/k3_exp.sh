@@ -1,5 +1,8 @@
 #!/bin/bash
-# K3 timing experiments: each experiment build (librsr_x*.so) vs librsr.so, k3_bench cases
+# K3 timing experiments: each experiment build (librsr_x*.so) vs librsr.so, k3_bench cases.
+# Experiment builds (CPU side, before the gpurun call), e.g. the weights-free consumer ceiling:
+#   python -c "import os,sys; sys.path.insert(0,'.'); from paper_1807_07433_b200 import build as b; \
+#              b.build(out=os.path.join(b.HERE,'librsr_xnow.so'), defines=['RSR_EXP_NOWCOMP'])"
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 TAG=${TAG:-k3x}
