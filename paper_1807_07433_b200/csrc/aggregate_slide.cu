@@ -130,6 +130,7 @@ struct SlideArgs {
   int R;                 // output rows per CTA (<= SG_SEGMAX)
   int nstrips;           // 32-column strips
   float kd, kr;
+  int hswap;             // clean path, G = 4: odd columns load their two halves in swapped order
   const float* vol;
   const void* guide;     // uint8 [B][H][W], or uint16 8.8 fixed point (G16)
   const uint8_t* nan_map;
@@ -410,17 +411,20 @@ __device__ __forceinline__ void produce_weights(const SlideArgs& A, const SlideG
 // (cost or 0, validity) of 4 disparities (NQ = 4); MODE 2: (cost or 0) pairs of 4
 // disparities with the per-pixel denominator (a half whose pixels are all fully
 // valid or skipped, NQ = 2).
+// oa (MODE 0): offset of the half loaded first (0, or 4G for a swapped column: with
+// G = 4 a quarter-warp of a 16-byte load spans two columns whose same halves sit in the
+// same 16 banks; swapping the odd column's halves makes the two columns' loads disjoint)
 template <int RHO, int MODE>
 RSR_DEVINL void slide_row(float2 (&acc)[2 * RHO + 1][4], float2 (&fin)[4], const float* crow,
-                          const float* wrow, int CS, int G) {
+                          const float* wrow, int CS, int G, int oa = 0) {
   constexpr int NT = 2 * RHO + 1;
   constexpr int NQ = MODE == 2 ? 2 : 4;
 #pragma unroll
   for (int j = 0; j < NT; j++) {
     float2 cp[4];
     if (MODE == 0) {
-      const float4 ca = *reinterpret_cast<const float4*>(crow + j * CS);
-      const float4 cb = *reinterpret_cast<const float4*>(crow + j * CS + 4 * G);
+      const float4 ca = *reinterpret_cast<const float4*>(crow + j * CS + oa);
+      const float4 cb = *reinterpret_cast<const float4*>(crow + j * CS + (4 * G - oa));
       cp[0] = make_float2(ca.x, ca.y); cp[1] = make_float2(ca.z, ca.w);
       cp[2] = make_float2(cb.x, cb.y); cp[3] = make_float2(cb.z, cb.w);
     } else {
@@ -511,6 +515,10 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
     }
     return;
   }
+  // clean path with G = 4: odd columns hold the upper half of their disparities in
+  // acc[.][0..1] and the lower half in acc[.][2..3] (bank-conflict-free cost loads)
+  const int sw = (CLEAN && A.hswap && g.G == 4) ? (xl & 1) : 0;
+  const int oa = sw ? 4 * g.G : 0;
   for (int pass = 0; pass < NPASS; pass++) {
     float2 acc[NT][4];
 #pragma unroll
@@ -532,7 +540,7 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
       RSR_CHECK(xl * g.XS + (NT - 1) * 16 + 16 <= 32 * g.XS && xl < 32);
       float2 fin[4];
       if (CLEAN)
-        slide_row<RHO, 0>(acc, fin, crow, wrow, g.CS, g.G);
+        slide_row<RHO, 0>(acc, fin, crow, wrow, g.CS, g.G, oa);
       else if (hc)
         slide_row<RHO, 2>(acc, fin, crow, wrow, g.CS, g.G);
       else
@@ -555,8 +563,8 @@ __device__ __forceinline__ void consume(const SlideArgs& A, const SlideGeom& g, 
                               fin[2].x * inv, fin[2].y * inv, fin[3].x * inv, fin[3].y * inv};
 #pragma unroll
           for (int hh = 0; hh < 2; hh++) {
-            const int kb = s.k0 + koff + 4 * g.G * hh;
-            float* oh = o + 4 * g.G * hh;
+            const int kb = s.k0 + koff + 4 * g.G * (hh ^ sw);
+            float* oh = o + 4 * g.G * (hh ^ sw);
             if (vec_out && kb + 3 < A.D) {
               *reinterpret_cast<float4*>(oh) = make_float4(r[4 * hh], r[4 * hh + 1], r[4 * hh + 2], r[4 * hh + 3]);
             } else {
@@ -766,6 +774,10 @@ static cudaError_t slide_launch_t(int B, int H, int W, int D, float gamma_d, flo
   A.kr = std::isinf(gamma_r) ? -1e-30f : -log2e / (gamma_r * gamma_r);
   if (G16) A.kr = std::isinf(gamma_r) ? 0.f : A.kr * (1.f / 65536.f);   // guide differences in 1/256 units
   A.vol = vol; A.guide = guide; A.nan_map = nan_map; A.out = out;
+  {
+    const char* e = getenv("RSR_K3_SWAP");   // experiment hook (tools/): 0 = unswapped loads
+    A.hswap = !(e && e[0] == '0');
+  }
   const long long nblk = cols * ((H + plan.R - 1) / plan.R);
   if (nblk > 0x7fffffffLL) return cudaErrorInvalidValue;
   auto kern = plan.minb == 1 ? k_aggregate_slide<RHO, 1, false, G16>
