@@ -314,9 +314,6 @@ def main(argv=None):
     dev = torch.device("cuda", local)
     distributed = "WORLD_SIZE" in os.environ
     if distributed:
-        # NCCL's version banner goes to stdout, ahead of rank 0's one JSON line
-        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-            os.environ["NCCL_DEBUG"] = "WARN"
         dist.init_process_group("nccl", device_id=dev)
     if world != args.gpus:
         log(f"bench: note: {world} rank(s) launched with --gpus {args.gpus}")

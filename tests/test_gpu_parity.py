@@ -387,6 +387,34 @@ def test_aggregate_independent_of_concurrency_hint(rsr):
         assert torch.equal(torch.nan_to_num(outs[0], nan=-7.0), torch.nan_to_num(o, nan=-7.0))
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("D,rho", [(30, 4), (32, 4), (26, 6), (32, 1)])
+def test_swapped_half_loads_bitwise_equal_unswapped(rsr, monkeypatch, D, rho):
+    """G = 4 slabs (25 <= D <= 32): odd columns of the clean path load (and store) their two
+    disparity halves in swapped order to avoid shared-memory bank conflicts; the values
+    are the same operations, so the maps agree bitwise with the unswapped loads
+    (RSR_K3_SWAP=0), on a c2-size frame with borders, warp bands and a constant patch."""
+    d_lo = -(D // 2)
+    cfg = synth.get_config("c2", d_lo=d_lo, d_hi=d_lo + D - 1, rho_agg=rho)
+    f = synth.make_frame(cfg)
+    L = torch.from_numpy(f.left)[None].cuda()
+    R = torch.from_numpy(f.right)[None].cuda()
+    L[0, 100:110, 200:210] = 77
+    ab = torch.tensor([[f.alpha, f.beta]], dtype=torch.float64, device="cuda")
+    W_, M_, S_ = rsr.rsr_warp(R, ab)
+    cl, cr, nl, nr = rsr.rsr_cost_volume(L, W_, M_, cfg.rho_block, cfg.d_lo, cfg.d_hi)
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("RSR_K3_SWAP", flag)
+        a = rsr.rsr_aggregate(cl, L, rho, cfg.gamma_d, cfg.gamma_r, nl)
+        b = rsr.rsr_aggregate(cr, W_, rho, cfg.gamma_d, cfg.gamma_r, nr)
+        torch.cuda.synchronize()
+        outs.append((a.cpu().numpy(), b.cpu().numpy()))
+    for x, y in zip(outs[0], outs[1]):
+        assert np.isfinite(x).any()
+        assert np.array_equal(x, y, equal_nan=True)
+
+
 @pytest.mark.parametrize("D,rho,with_nan_map", [(8, 6, True), (8, 6, False), (3, 2, True), (5, 7, True),
                                                (9, 4, True), (12, 6, False), (16, 3, True), (6, 0, True)])
 def test_small_slab_kernel_bitwise_equals_sliding_kernel(rsr, monkeypatch, D, rho, with_nan_map):
