@@ -13,7 +13,9 @@
 //    does not depend on k, so all lanes of a group read the SAME weight
 //    address: one LDS.128 broadcast serves 4 weights to 4 groups (one
 //    shared-memory wavefront), each weight feeding 64 FMAs.  Cost loads are
-//    per lane and contiguous (8 lanes x 16 B = one 128-B row per group).
+//    per lane and contiguous (8 lanes x 16 B = one 128-B row per group); with
+//    G = 4 the odd columns load their two halves in swapped order, so the two
+//    columns of a quarter-warp never share banks.
 //  * The strip slides down one input row at a time.  A thread keeps the
 //    2 rho + 1 output rows whose windows contain the current input row
 //    ("ages") x 8 disparities as packed pairs (104 registers at rho = 6), so
